@@ -1,0 +1,205 @@
+/* sketchmp.h — C-ABI of the B200-native sketch + matrix-profile hot path of
+ * "Sketching Multidimensional Time Series for Fast Discord Mining" (arXiv 2311.03393).
+ *
+ * Citation key: "P:L<a>-<b>" = PAPER.md lines (section / definition / algorithm given);
+ * "reading N" = the numbered paper-gap readings in DESIGN.md §3.
+ *
+ * General rules (all entry points):
+ *  - Every call returns skmp_status; nothing throws, exits or prints.  On a non-OK status
+ *    skmp_last_error() holds a thread-local message and skmp_last_error_index() the offending
+ *    stream / group / row (or -1).  All argument validation happens before any launch; on an
+ *    error status caller-owned output buffers are left untouched.
+ *  - "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).  Device work is
+ *    enqueued on it in order.  Calls documented as "synchronous" wait for their own work.
+ *  - Pointers tagged [dev] must be device (HBM) memory of the current CUDA device; [host] must be
+ *    host memory; [dev|host] accepts either (detected with cudaPointerGetAttributes; a host
+ *    buffer is staged to HBM inside the call, which then is synchronous).
+ *  - Matrices are row-major: element (r, c) of a rows x cols matrix with leading dimension ld
+ *    lives at base[r*ld + c]; ld is in elements.
+ *  - dtype: SKMP_F32 or SKMP_F64 gives the element type of T, R and P; FP32 paths accumulate
+ *    the sketch and all window statistics in FP64 (reading 14).
+ *  - There is no CPU fallback: without a CUDA device every compute call returns SKMP_E_CUDA.
+ */
+#ifndef SKETCHMP_H
+#define SKETCHMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKMP_ABI_VERSION 1
+
+typedef enum {
+  SKMP_OK = 0,
+  SKMP_E_INVALID_ARG = 1,      /* NULL, d<1, k<1, m<2, ld<n, top<1, bad dtype/proj/band     */
+  SKMP_E_CONSTANT_SERIES = 2,  /* sigma_j <= 1e-12 (max|x|+1)            reading 4   */
+  SKMP_E_NONFINITE = 3,        /* NaN/Inf in an input stream                                  */
+  SKMP_E_SERIES_TOO_SHORT = 4, /* n < m                                     (Def. 2)   */
+  SKMP_E_NO_ADMISSIBLE = 5,    /* n_sub < 2*excl+2: some row has no |i-j| > excl  reading 7   */
+  SKMP_E_DUPLICATE_DIM = 6,    /* id already in the sketch      */
+  SKMP_E_UNKNOWN_DIM = 7,      /* delete of an id that is not in the sketch                   */
+  SKMP_E_LENGTH_MISMATCH = 8,  /* added/deleted streams must span the full n     */
+  SKMP_E_ALL_GROUPS_INERT = 9, /* every sketch group empty or flat         reading 10         */
+  SKMP_E_CUDA = 10,            /* CUDA runtime error (incl. no device)                         */
+  SKMP_E_NCCL = 11,            /* reserved: collective errors (multi-GPU reduce lives above)  */
+  SKMP_E_OOM = 12              /* device allocation failed                                     */
+} skmp_status;
+
+typedef enum { SKMP_F32 = 0, SKMP_F64 = 1 } skmp_dtype;
+typedef enum { SKMP_PROJ_COUNT_SKETCH = 0, SKMP_PROJ_DENSE = 1 } skmp_proj;
+
+/* ---------------------------------------------------------------------------------------------
+ * Errors / version (host-only; callable without a GPU)
+ * ------------------------------------------------------------------------------------------- */
+const char* skmp_status_string(skmp_status s);   /* static string                              */
+const char* skmp_last_error(void);               /* thread-local text of the last non-OK call  */
+int64_t skmp_last_error_index(void);             /* offending stream/group/row, or -1          */
+int32_t skmp_abi_version(void);                  /* SKMP_ABI_VERSION                           */
+
+/* ---------------------------------------------------------------------------------------------
+ * Hash plan (host-only; callable without a GPU).  The count-sketch pair (h, s) of P:L200-204
+ * (§3.1: "two pair-wise independent hash functions h: [d]->[k] and s: [d]->{-1,+1}").
+ * Reading 2: Carter–Wegman over p = 2^61-1 keyed by the stream id, parameters (a, b, c, e) from
+ * splitmix64(seed): h(id) = ((a x + b) mod p) mod k,  s(id) = +1 iff ((c x + e) mod p) is even,
+ * x = id mod p.
+ *   ids    [host] d stream ids          groups [host, out] d ints in [0,k)   signs [host, out] d
+ * Errors: INVALID_ARG (NULL, d<0, k<1).
+ * ------------------------------------------------------------------------------------------- */
+skmp_status sketch_hash_plan(const uint64_t* ids, int64_t d, int32_t k, uint64_t seed,
+                             int32_t* groups, int8_t* signs);
+
+/* ---------------------------------------------------------------------------------------------
+ * Sketch (Alg. 1; z-normalisation P:L210; linear updates §3.3)
+ *
+ *   R^(g) = sum_{j in J_g} s(j) * (T_j - mu_j) / sigma_j,   J_g = { j : h(j) = g }
+ *
+ * with mu_j, sigma_j the stream's own whole-series mean and population std (reading 3), summed
+ * in FP64 in ascending input order inside each group and rounded once to dtype.  DENSE instead
+ * computes R = S * diag(1/sigma) * (T - mu) for a caller matrix S (reading 1).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct skmp_sketch skmp_sketch;   /* opaque; owns R (k x n) and the per-dim plan      */
+
+typedef struct {
+  int32_t k;              /* number of sketch series (groups), >= 1                            */
+  int32_t dtype;          /* skmp_dtype of T and R                                             */
+  int32_t proj;           /* skmp_proj                                                         */
+  int32_t reserved;       /* must be 0                                                         */
+  uint64_t seed;          /* hash seed (COUNT_SKETCH)                                          */
+  const int32_t* groups;  /* optional [host] d: explicit h (test hook, e.g. identity plan)     */
+  const int8_t* signs;    /* optional [host] d: explicit s (+1/-1); requires groups            */
+  const double* S;        /* DENSE only, [host] k x d row-major (copied)                       */
+} skmp_sketch_cfg;
+
+/* Build the sketch of T (d streams of n samples, leading dimension ld).
+ *   T    [dev|host] d x ld (dtype); only the first n columns are read.   ids [host] d, unique.
+ *   out  receives a new handle (free with sketch_free).
+ * Two HBM passes over T (stream statistics, then projection).  One small synchronous D2H of
+ * error flags.  Errors: INVALID_ARG, NONFINITE, CONSTANT_SERIES (index = stream row),
+ * DUPLICATE_DIM, CUDA, OOM. */
+skmp_status sketch_build(const void* T, int64_t d, int64_t n, int64_t ld, const uint64_t* ids,
+                         const skmp_sketch_cfg* cfg, void* stream, skmp_sketch** out);
+
+/* Add nb full-length streams (P:L329-334 linearity; must span all n samples).
+ *   T [dev|host] nb x ld;  ids [host] nb (new, unique);  S_cols [host] k x nb for DENSE, else NULL.
+ * R^(h(j)) += s(j) z_j in FP64 (the handle keeps FP64 master accumulators), then R = dtype(R64).
+ * Errors: INVALID_ARG, DUPLICATE_DIM, NONFINITE, CONSTANT_SERIES, CUDA, OOM. */
+skmp_status sketch_add_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld,
+                           const uint64_t* ids, const double* S_cols, void* stream);
+
+/* Delete nb streams (R^(g) = R^(g) - s(j) T^(j)).  The caller re-supplies the raw
+ * streams (the sketch keeps none); their STORED mu/sigma are used, so add-then-delete is an exact
+ * inverse up to one FP64 rounding.  Errors: INVALID_ARG, UNKNOWN_DIM, CUDA, OOM. */
+skmp_status sketch_del_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld,
+                           const uint64_t* ids, void* stream);
+
+/* Borrowed views (valid until the next add/del/free).  R: [dev] k x n, ld = n, dtype.
+ * R64: [dev] k x n FP64 master accumulators. */
+skmp_status sketch_view(const skmp_sketch* h, const void** R, int32_t* k, int64_t* n, int64_t* d,
+                        int32_t* dtype);
+skmp_status sketch_view64(const skmp_sketch* h, const double** R64);
+
+/* Copy the current plan to host arrays of length d (any may be NULL): ids, group, sign,
+ * mu, sigma (sign is 0 and group -1 for DENSE). */
+skmp_status sketch_plan(const skmp_sketch* h, uint64_t* ids, int32_t* g, int8_t* s, double* mu,
+                        double* sigma);
+void sketch_free(skmp_sketch* h);
+
+/* ---------------------------------------------------------------------------------------------
+ * Matrix-profile self-join over each sketch series (Def. 6; self-join variant
+ * P:L322; dist = z-normalised Euclidean, Def. 3):
+ *
+ *   P_g[i] = min_{ j : |i-j| > excl } dist(R^(g)_{i,m}, R^(g)_{j,m}),  I_g[i] = smallest argmin
+ *
+ * excl = ceil(m/2) by default (reading 7).  Flat windows (sigma <= 1e-12 (max|R_g|+1)) follow
+ * reading 5 (flat-flat 0, flat vs non-flat sqrt(m)); a group whose windows are all flat is
+ * "inert" (reading 6): P_g = 0 and inert[g] = 1.
+ * Computed by the STOMP/SCAMP diagonal recurrence on mean-centred dot products with exact FP64
+ * re-seeding every `reseed_rows` rows; the chosen neighbour's distance is then recomputed
+ * exactly in FP64.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t m;            /* subsequence length, >= 2                                          */
+  int32_t excl;         /* exclusion radius; < 0 -> ceil(m/2)                                 */
+  int32_t reseed_rows;  /* 0 -> default (FP32 8192, FP64 2048); rounded up to 64              */
+  int32_t reserved;     /* must be 0                                                          */
+} skmp_mp_cfg;
+
+typedef struct skmp_mp skmp_mp;  /* opaque join workspace: window statistics + profile keys */
+
+/* Window preparation (per-window mean/std in FP64 by direct sums, flat flags, recurrence terms)
+ * and key initialisation.  R [dev] k x ld (dtype), n samples per series.  Synchronous (one D2H
+ * of per-series flat counts).  Errors: INVALID_ARG, SERIES_TOO_SHORT, NO_ADMISSIBLE, CUDA, OOM.*/
+skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                      const skmp_mp_cfg* cfg, void* stream, skmp_mp** out);
+
+/* Accumulate the join over diagonals [diag_lo, diag_hi) (0,0 -> all of [excl+1, n_sub)) into
+ * the workspace's keys.  Bands are disjoint diagonal ranges; any partition of [excl+1, n_sub)
+ * accumulates bit-identical keys (band edges are rounded to the tile width, see mp_band).
+ * Asynchronous.  Errors: INVALID_ARG, CUDA. */
+skmp_status mp_join(skmp_mp* w, int64_t diag_lo, int64_t diag_hi, void* stream);
+
+/* Device view of the profile keys, for a cross-GPU max-reduce (multi-GPU bands):
+ *   keys [dev] count int64 words, `words` per profile entry (FP32: 1, FP64: 2);
+ * FP32 word = (orderable(rho_f32) << 32) | (0xFFFFFFFF - j); FP64 words = {orderable(rho_f64),
+ * -1 - j}.  Larger is better (max rho, then smallest j): FP32 keys reduce with one signed int64
+ * MAX; FP64 keys reduce lexicographically (MAX of word 0, then MAX of word 1 among ties). */
+skmp_status mp_keys(skmp_mp* w, void** keys, int64_t* count, int32_t* words);
+
+/* Host-only: diagonal band `band` of `nbands` equal-cell bands of [excl+1, n_sub), edges
+ * rounded to the join's tile width for dtype (so band results are bit-identical to a single
+ * join).  Errors: INVALID_ARG. */
+skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, int32_t band,
+                    int64_t* diag_lo, int64_t* diag_hi);
+
+/* Finalize: keys -> P [dev] k x n_sub (dtype) and I [dev] k x n_sub (int64), inert [host] k.
+ * Requires the full diagonal range to have been joined.  Synchronous only for the inert copy.
+ * Errors: INVALID_ARG, CUDA. */
+skmp_status mp_finalize(skmp_mp* w, void* P, int64_t* I, uint8_t* inert, void* stream);
+void mp_free(skmp_mp* w);
+
+/* One-shot: mp_create + mp_join(all) + mp_finalize + mp_free. */
+skmp_status mp_selfjoin(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                        const skmp_mp_cfg* cfg, void* P, int64_t* I, uint8_t* inert, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Discord detection over the sketch profiles: Alg. 2 Time-Detection + ordered
+ * top-K list (reading 12):
+ *   C[i] = max_{g not inert} P_g[i], G[i] = smallest maximising g (Alg. 2 strict '>' P:L262);
+ *   repeat top times: t = smallest-index argmax of C over unmasked windows; emit
+ *   (t, G[t], I_G[t][t], C[t]); mask [t - radius, t + radius].
+ *   P [dev] k x ldp (dtype), I [dev] k x ldp, inert [host] k (NULL = none inert).
+ *   radius < 0 -> ceil(m/2).  t_out/g_out/nn_out/score_out [host] top entries; n_found [host]
+ *   receives the number emitted (< top when the mask exhausts the profile).  Synchronous.
+ * Errors: INVALID_ARG, ALL_GROUPS_INERT, CUDA, OOM. */
+skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, int32_t k,
+                         int64_t n_sub, int64_t ldp, int32_t m, int32_t dtype, int32_t top,
+                         int32_t radius, int64_t* t_out, int32_t* g_out, int64_t* nn_out,
+                         double* score_out, int32_t* n_found, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHMP_H */
