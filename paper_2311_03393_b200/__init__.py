@@ -1,0 +1,382 @@
+"""Thin Python binding of the sketch + matrix-profile C-ABI (include/sketchmp.h).
+
+Argument marshalling only: every step of the path runs in libsketchmp.so's CUDA kernels.
+PyTorch supplies device memory and the current CUDA stream.  The same names as the C-ABI:
+
+    sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
+    sketch_plan, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
+    mp_selfjoin, discord_topk
+
+There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
+without a GPU return SKMP_E_CUDA (raised as SkmpError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsketchmp.so")
+
+F32, F64 = 0, 1
+PROJ_COUNT_SKETCH, PROJ_DENSE = 0, 1
+
+STATUS = {
+    0: "SKMP_OK", 1: "SKMP_E_INVALID_ARG", 2: "SKMP_E_CONSTANT_SERIES", 3: "SKMP_E_NONFINITE",
+    4: "SKMP_E_SERIES_TOO_SHORT", 5: "SKMP_E_NO_ADMISSIBLE", 6: "SKMP_E_DUPLICATE_DIM",
+    7: "SKMP_E_UNKNOWN_DIM", 8: "SKMP_E_LENGTH_MISMATCH", 9: "SKMP_E_ALL_GROUPS_INERT",
+    10: "SKMP_E_CUDA", 11: "SKMP_E_NCCL", 12: "SKMP_E_OOM",
+}
+
+
+class SkmpError(RuntimeError):
+    def __init__(self, status: int, message: str, index: int):
+        super().__init__(f"{STATUS.get(status, status)}: {message} (index {index})")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        self.message = message
+        self.index = index
+
+
+class SketchCfg(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("proj", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("groups", ctypes.c_void_p), ("signs", ctypes.c_void_p), ("S", ctypes.c_void_p)]
+
+
+class MpCfg(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("excl", ctypes.c_int32), ("reseed_rows", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+
+_SIGS = {
+    "skmp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "skmp_last_error": (ctypes.c_char_p, []),
+    "skmp_last_error_index": (_I64, []),
+    "skmp_abi_version": (_I32, []),
+    "sketch_hash_plan": (ctypes.c_int, [_P, _I64, _I32, ctypes.c_uint64, _P, _P]),
+    "sketch_build": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, ctypes.POINTER(SketchCfg), _P, ctypes.POINTER(_P)]),
+    "sketch_add_dim": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
+    "sketch_del_dim": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P]),
+    "sketch_view": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I32), ctypes.POINTER(_I64),
+                                   ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+    "sketch_view64": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "sketch_plan": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "sketch_free": (None, [_P]),
+    "mp_create": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, ctypes.POINTER(_P)]),
+    "mp_join": (ctypes.c_int, [_P, _I64, _I64, _P]),
+    "mp_keys": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+    "mp_band": (ctypes.c_int, [_I64, _I32, _I32, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "mp_finalize": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "mp_free": (None, [_P]),
+    "mp_selfjoin": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
+    "discord_topk": (ctypes.c_int, [_P, _P, _P, _I32, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
+                                    _P, _P]),
+}
+
+
+def lib():
+    """Load libsketchmp.so (fails loudly if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2311_03393_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        L = lib()
+        raise SkmpError(st, L.skmp_last_error().decode(), int(L.skmp_last_error_index()))
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    import torch
+    if torch.cuda.is_available():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+def _ptr(x):
+    """data pointer of a torch tensor / numpy array / int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr())
+    return ctypes.c_void_p(x.ctypes.data)
+
+
+def _dtype_code(t) -> int:
+    s = str(getattr(t, "dtype", t))
+    if "float32" in s:
+        return F32
+    if "float64" in s:
+        return F64
+    raise ValueError(f"unsupported dtype {s} (float32 / float64)")
+
+
+class _DevArray:
+    """Zero-copy view of library-owned device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _as_tensor(ptr: int, shape, dtype_code: int):
+    import torch
+    ts = "<f4" if dtype_code == F32 else "<f8"
+    return torch.as_tensor(_DevArray(ptr, shape, ts), device="cuda")
+
+
+# ----------------------------------------------------------------------------------------------
+# host-only
+# ----------------------------------------------------------------------------------------------
+
+def sketch_hash_plan(ids, k: int, seed: int):
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    g = np.empty(len(ids), dtype=np.int32)
+    s = np.empty(len(ids), dtype=np.int8)
+    _check(lib().sketch_hash_plan(_ptr(ids), len(ids), k, seed, _ptr(g), _ptr(s)))
+    return g, s
+
+
+def mp_band(n_sub: int, excl: int, dtype: int, nbands: int, band: int):
+    lo, hi = _I64(), _I64()
+    _check(lib().mp_band(n_sub, excl, dtype, nbands, band, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+# ----------------------------------------------------------------------------------------------
+# sketch
+# ----------------------------------------------------------------------------------------------
+
+class Sketch:
+    """Owning wrapper of a skmp_sketch handle."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def free(self):
+        if self.handle:
+            lib().sketch_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    @property
+    def R(self):
+        return sketch_view(self)[0]
+
+    @property
+    def R64(self):
+        return sketch_view64(self)
+
+
+def sketch_build(T, ids, k: int, *, seed: int = 0, proj: int = PROJ_COUNT_SKETCH, groups=None,
+                 signs=None, S=None, stream=None, n: int | None = None) -> Sketch:
+    """T: d x ld tensor/array (CUDA tensor or host array/tensor, float32/float64)."""
+    d = T.shape[0]
+    ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+    n = T.shape[1] if n is None else n
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    cfg = SketchCfg()
+    cfg.k = k
+    cfg.dtype = _dtype_code(T)
+    cfg.proj = proj
+    cfg.seed = seed
+    keep = []
+    if groups is not None:
+        g = np.ascontiguousarray(groups, dtype=np.int32)
+        keep.append(g)
+        cfg.groups = g.ctypes.data
+    if signs is not None:
+        s = np.ascontiguousarray(signs, dtype=np.int8)
+        keep.append(s)
+        cfg.signs = s.ctypes.data
+    if S is not None:
+        Sm = np.ascontiguousarray(S, dtype=np.float64)
+        keep.append(Sm)
+        cfg.S = Sm.ctypes.data
+    h = ctypes.c_void_p()
+    _check(lib().sketch_build(_ptr(T), d, n, ld, _ptr(ids), ctypes.byref(cfg), _stream(stream), ctypes.byref(h)))
+    return Sketch(h)
+
+
+def sketch_add_dim(sk: Sketch, T, ids, S_cols=None, stream=None):
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+    Sc = None if S_cols is None else np.ascontiguousarray(S_cols, dtype=np.float64)
+    _check(lib().sketch_add_dim(sk.handle, _ptr(T), T.shape[0], ld, _ptr(ids), _ptr(Sc), _stream(stream)))
+
+
+def sketch_del_dim(sk: Sketch, T, ids, stream=None):
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+    _check(lib().sketch_del_dim(sk.handle, _ptr(T), T.shape[0], ld, _ptr(ids), _stream(stream)))
+
+
+def sketch_view(sk: Sketch):
+    """(R as a zero-copy torch CUDA tensor k x n, k, n, d, dtype)."""
+    R, k, n, d, dt = _P(), _I32(), _I64(), _I64(), _I32()
+    _check(lib().sketch_view(sk.handle, ctypes.byref(R), ctypes.byref(k), ctypes.byref(n), ctypes.byref(d),
+                             ctypes.byref(dt)))
+    return _as_tensor(R.value, (k.value, n.value), dt.value), k.value, n.value, d.value, dt.value
+
+
+def sketch_view64(sk: Sketch):
+    p = _P()
+    _check(lib().sketch_view64(sk.handle, ctypes.byref(p)))
+    _, k, n, _, _ = sketch_view(sk)
+    return _as_tensor(p.value, (k, n), F64)
+
+
+def sketch_plan(sk: Sketch):
+    _, k, n, d, _ = sketch_view(sk)
+    ids = np.empty(d, np.uint64)
+    g = np.empty(d, np.int32)
+    s = np.empty(d, np.int8)
+    mu = np.empty(d)
+    sg = np.empty(d)
+    _check(lib().sketch_plan(sk.handle, _ptr(ids), _ptr(g), _ptr(s), _ptr(mu), _ptr(sg)))
+    return dict(ids=ids, groups=g, signs=s, mu=mu, sigma=sg)
+
+
+def sketch_free(sk: Sketch):
+    sk.free()
+
+
+# ----------------------------------------------------------------------------------------------
+# matrix profile
+# ----------------------------------------------------------------------------------------------
+
+def _mpcfg(m: int, excl: int = -1, reseed_rows: int = 0) -> MpCfg:
+    c = MpCfg()
+    c.m = m
+    c.excl = excl
+    c.reseed_rows = reseed_rows
+    return c
+
+
+class MpWorkspace:
+    def __init__(self, handle, k: int, n_sub: int, dtype: int):
+        self.handle, self.k, self.n_sub, self.dtype = handle, k, n_sub, dtype
+
+    def free(self):
+        if self.handle:
+            lib().mp_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def mp_create(R, m: int, *, excl: int = -1, reseed_rows: int = 0, n: int | None = None, stream=None) -> MpWorkspace:
+    k = R.shape[0]
+    n = R.shape[1] if n is None else n
+    ld = R.stride(0)
+    dt = _dtype_code(R)
+    cfg = _mpcfg(m, excl, reseed_rows)
+    h = ctypes.c_void_p()
+    _check(lib().mp_create(_ptr(R), k, n, ld, dt, ctypes.byref(cfg), _stream(stream), ctypes.byref(h)))
+    return MpWorkspace(h, k, n - m + 1, dt)
+
+
+def mp_join(w: MpWorkspace, diag_lo: int = 0, diag_hi: int = 0, stream=None):
+    _check(lib().mp_join(w.handle, diag_lo, diag_hi, _stream(stream)))
+
+
+def mp_keys(w: MpWorkspace):
+    """Zero-copy int64 torch view of the profile keys (k*n_sub*words)."""
+    import torch
+    p, cnt, words = _P(), _I64(), _I32()
+    _check(lib().mp_keys(w.handle, ctypes.byref(p), ctypes.byref(cnt), ctypes.byref(words)))
+    arr = _DevArray(p.value, (cnt.value,), "<i8")
+    return torch.as_tensor(arr, device="cuda"), words.value
+
+
+def mp_finalize(w: MpWorkspace, P=None, I=None, stream=None):
+    import torch
+    tdt = torch.float32 if w.dtype == F32 else torch.float64
+    if P is None:
+        P = torch.empty((w.k, w.n_sub), dtype=tdt, device="cuda")
+    if I is None:
+        I = torch.empty((w.k, w.n_sub), dtype=torch.int64, device="cuda")
+    inert = np.zeros(w.k, dtype=np.uint8)
+    _check(lib().mp_finalize(w.handle, _ptr(P), _ptr(I), _ptr(inert), _stream(stream)))
+    return P, I, inert.astype(bool)
+
+
+def mp_free(w: MpWorkspace):
+    w.free()
+
+
+def mp_selfjoin(R, m: int, *, excl: int = -1, reseed_rows: int = 0, n: int | None = None, P=None, I=None,
+                stream=None):
+    """R: k x ld CUDA tensor.  Returns (P k x n_sub, I k x n_sub int64, inert bool[k])."""
+    import torch
+    k = R.shape[0]
+    n = R.shape[1] if n is None else n
+    n_sub = n - m + 1
+    dt = _dtype_code(R)
+    tdt = torch.float32 if dt == F32 else torch.float64
+    if P is None:
+        P = torch.empty((k, max(n_sub, 1)), dtype=tdt, device=R.device)
+    if I is None:
+        I = torch.empty((k, max(n_sub, 1)), dtype=torch.int64, device=R.device)
+    inert = np.zeros(k, dtype=np.uint8)
+    cfg = _mpcfg(m, excl, reseed_rows)
+    _check(lib().mp_selfjoin(_ptr(R), k, n, R.stride(0), dt, ctypes.byref(cfg), _ptr(P), _ptr(I), _ptr(inert),
+                             _stream(stream)))
+    return P, I, inert.astype(bool)
+
+
+# ----------------------------------------------------------------------------------------------
+# detection
+# ----------------------------------------------------------------------------------------------
+
+@dataclass
+class Discord:
+    t: int
+    g: int
+    nn: int
+    score: float
+
+
+def discord_topk(P, I, inert, m: int, top: int, radius: int = -1, stream=None) -> list[Discord]:
+    k, n_sub = P.shape
+    inert_a = None if inert is None else np.ascontiguousarray(inert, dtype=np.uint8)
+    t = np.empty(top, np.int64)
+    g = np.empty(top, np.int32)
+    nn = np.empty(top, np.int64)
+    sc = np.empty(top, np.float64)
+    nf = _I32()
+    _check(lib().discord_topk(_ptr(P), _ptr(I), _ptr(inert_a), k, n_sub, P.stride(0), m, _dtype_code(P), top,
+                              radius, _ptr(t), _ptr(g), _ptr(nn), _ptr(sc), ctypes.byref(nf), _stream(stream)))
+    return [Discord(int(t[q]), int(g[q]), int(nn[q]), float(sc[q])) for q in range(nf.value)]

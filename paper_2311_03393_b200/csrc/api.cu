@@ -1,0 +1,759 @@
+// C-ABI layer (include/sketchmp.h): validation, handles, plans, host<->device plumbing and
+// launch sequencing.  Every step of the path itself runs in the kernels of sketch.cu,
+// mp_prep.cu, mp_join.cu, mp_final.cu and detect.cu; there is no CPU fallback.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "internal.h"
+
+// ============================================================================================
+// errors
+// ============================================================================================
+namespace {
+thread_local std::string g_msg;
+thread_local int64_t g_index = -1;
+}  // namespace
+
+namespace skmp {
+skmp_status set_error(skmp_status s, const std::string& msg, int64_t index) {
+  g_msg = msg;
+  g_index = index;
+  return s;
+}
+skmp_status cuda_error(cudaError_t e, const char* where) {
+  const skmp_status s = (e == cudaErrorMemoryAllocation) ? SKMP_E_OOM : SKMP_E_CUDA;
+  return set_error(s, std::string(where) + ": " + cudaGetErrorString(e), -1);
+}
+}  // namespace skmp
+
+using namespace skmp;
+
+namespace {
+
+skmp_status ok() {
+  g_msg.clear();
+  g_index = -1;
+  return SKMP_OK;
+}
+
+skmp_status require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return set_error(SKMP_E_CUDA, "no CUDA device available (the path has no CPU fallback)");
+  }
+  return SKMP_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t elem_size(int dtype) { return dtype == SKMP_F32 ? 4 : 8; }
+
+// RAII list of stream-ordered temporaries
+struct Temps {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Temps(cudaStream_t s) : st(s) {}
+  ~Temps() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, st);
+    if (e == cudaSuccess) {
+      ptrs.push_back(q);
+      *p = static_cast<T*>(q);
+    }
+    return e;
+  }
+};
+
+// Stage a (possibly host) rows x ld matrix into device memory; returns the device pointer.
+skmp_status stage_input(const void* T, int64_t rows, int64_t n, int64_t ld, int dtype, Temps& tmp,
+                        const void** dev, int64_t* dev_ld) {
+  if (is_device_ptr(T)) {
+    *dev = T;
+    *dev_ld = ld;
+    return SKMP_OK;
+  }
+  const size_t es = elem_size(dtype);
+  char* d = nullptr;
+  SKMP_CUDA(tmp.alloc(&d, (size_t)rows * (size_t)n * es));
+  SKMP_CUDA(cudaMemcpy2DAsync(d, (size_t)n * es, T, (size_t)ld * es, (size_t)n * es, (size_t)rows,
+                              cudaMemcpyHostToDevice, tmp.st));
+  *dev = d;
+  *dev_ld = n;
+  return SKMP_OK;
+}
+
+template <typename T>
+skmp_status upload(const std::vector<T>& h, T** d, Temps& tmp) {
+  SKMP_CUDA(tmp.alloc(d, h.size() ? h.size() : 1));
+  if (!h.empty())
+    SKMP_CUDA(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, tmp.st));
+  return SKMP_OK;
+}
+
+struct StatsHost {
+  std::vector<double> mu, sigma;
+};
+
+// K1 on rows of T, then one small synchronous D2H of mu/sigma/flags; maps flags to errors.
+skmp_status run_stats(const void* Tdev, int64_t rows, int64_t n, int64_t ld, int dtype, Temps& tmp,
+                      StatsHost* out, double** d_mu, double** d_inv) {
+  StatsOut so;
+  double* buf = nullptr;
+  SKMP_CUDA(tmp.alloc(&buf, (size_t)rows * 3));
+  int32_t* flag = nullptr;
+  SKMP_CUDA(tmp.alloc(&flag, (size_t)rows));
+  void* ws = nullptr;
+  char* wsc = nullptr;
+  SKMP_CUDA(tmp.alloc(&wsc, stats_ws_bytes(rows, n)));
+  ws = wsc;
+  so.mu = buf;
+  so.sigma = buf + rows;
+  so.inv = buf + 2 * rows;
+  so.flag = flag;
+  SKMP_CUDA(launch_stream_stats(Tdev, rows, n, ld, dtype, so, ws, tmp.st));
+  std::vector<int32_t> hf((size_t)rows);
+  out->mu.resize((size_t)rows);
+  out->sigma.resize((size_t)rows);
+  SKMP_CUDA(cudaMemcpyAsync(hf.data(), flag, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, tmp.st));
+  SKMP_CUDA(cudaMemcpyAsync(out->mu.data(), so.mu, sizeof(double) * rows, cudaMemcpyDeviceToHost, tmp.st));
+  SKMP_CUDA(cudaMemcpyAsync(out->sigma.data(), so.sigma, sizeof(double) * rows, cudaMemcpyDeviceToHost, tmp.st));
+  SKMP_CUDA(cudaStreamSynchronize(tmp.st));
+  for (int64_t j = 0; j < rows; ++j) {
+    if (hf[(size_t)j] == 1) return set_error(SKMP_E_NONFINITE, "non-finite value in input stream", j);
+    if (hf[(size_t)j] == 2)
+      return set_error(SKMP_E_CONSTANT_SERIES, "constant input stream (sigma <= 1e-12 (max|x|+1))", j);
+  }
+  *d_mu = so.mu;
+  *d_inv = so.inv;
+  return SKMP_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+// sketch handle
+// ============================================================================================
+struct skmp_sketch {
+  int dtype = SKMP_F32;
+  int proj = SKMP_PROJ_COUNT_SKETCH;
+  int k = 0;
+  int64_t n = 0;
+  uint64_t seed = 0;
+  double* R64 = nullptr;  // k x n
+  void* R = nullptr;      // k x n (== R64 for FP64)
+  cudaStream_t st = nullptr;
+  std::vector<uint64_t> ids;
+  std::vector<int32_t> g;
+  std::vector<int8_t> s;
+  std::vector<double> mu, sigma;
+  std::vector<double> Scol;  // DENSE: d columns of length k (column-major per stream)
+  std::unordered_map<uint64_t, int64_t> pos;
+};
+
+namespace {
+
+// project rows [0, rows) of Tdev into the handle with mode 0/+1/-1
+skmp_status project_rows(skmp_sketch* h, const void* Tdev, int64_t ld, int64_t rows,
+                         const std::vector<int32_t>& gg, const std::vector<int8_t>& ss,
+                         const std::vector<double>& Scols, const std::vector<double>& mu,
+                         const std::vector<double>& sigma, int mode, Temps& tmp) {
+  std::vector<double> inv((size_t)rows);
+  for (int64_t j = 0; j < rows; ++j) inv[(size_t)j] = 1.0 / sigma[(size_t)j];
+  if (h->proj == SKMP_PROJ_COUNT_SKETCH) {
+    // CSR: group g -> rows in ascending input order (Alg. 1 loop order inside each group)
+    std::vector<int32_t> off((size_t)h->k + 1, 0), row((size_t)rows);
+    std::vector<double> cmu((size_t)rows), cinv((size_t)rows);
+    std::vector<int8_t> csg((size_t)rows);
+    for (int64_t j = 0; j < rows; ++j) off[(size_t)gg[(size_t)j] + 1]++;
+    for (int q = 0; q < h->k; ++q) off[(size_t)q + 1] += off[(size_t)q];
+    std::vector<int32_t> fill(off.begin(), off.end() - 1);
+    for (int64_t j = 0; j < rows; ++j) {
+      const int32_t e = fill[(size_t)gg[(size_t)j]]++;
+      row[(size_t)e] = (int32_t)j;
+      cmu[(size_t)e] = mu[(size_t)j];
+      cinv[(size_t)e] = inv[(size_t)j];
+      csg[(size_t)e] = ss[(size_t)j];
+    }
+    CsrPlan p;
+    int32_t *d_off, *d_row;
+    double *d_mu, *d_inv;
+    int8_t* d_sg;
+    skmp_status s;
+    if ((s = upload(off, &d_off, tmp)) != SKMP_OK) return s;
+    if ((s = upload(row, &d_row, tmp)) != SKMP_OK) return s;
+    if ((s = upload(cmu, &d_mu, tmp)) != SKMP_OK) return s;
+    if ((s = upload(cinv, &d_inv, tmp)) != SKMP_OK) return s;
+    if ((s = upload(csg, &d_sg, tmp)) != SKMP_OK) return s;
+    p.off = d_off;
+    p.row = d_row;
+    p.mu = d_mu;
+    p.inv = d_inv;
+    p.sign = d_sg;
+    SKMP_CUDA(launch_project_count(Tdev, ld, h->n, h->dtype, h->k, p, mode, h->R64, h->R, tmp.st));
+  } else {
+    // dense S as k x rows row-major for the kernel
+    std::vector<double> S((size_t)h->k * (size_t)rows);
+    for (int64_t j = 0; j < rows; ++j)
+      for (int q = 0; q < h->k; ++q) S[(size_t)q * rows + j] = Scols[(size_t)j * h->k + q];
+    double *d_S, *d_mu, *d_inv;
+    skmp_status s;
+    if ((s = upload(S, &d_S, tmp)) != SKMP_OK) return s;
+    if ((s = upload(mu, &d_mu, tmp)) != SKMP_OK) return s;
+    if ((s = upload(inv, &d_inv, tmp)) != SKMP_OK) return s;
+    SKMP_CUDA(launch_project_dense(Tdev, ld, h->n, h->dtype, h->k, rows, d_S, rows, d_mu, d_inv,
+                                   mode, h->R64, h->R, tmp.st));
+  }
+  return SKMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skmp_status_string(skmp_status s) {
+  switch (s) {
+    case SKMP_OK: return "SKMP_OK";
+    case SKMP_E_INVALID_ARG: return "SKMP_E_INVALID_ARG";
+    case SKMP_E_CONSTANT_SERIES: return "SKMP_E_CONSTANT_SERIES";
+    case SKMP_E_NONFINITE: return "SKMP_E_NONFINITE";
+    case SKMP_E_SERIES_TOO_SHORT: return "SKMP_E_SERIES_TOO_SHORT";
+    case SKMP_E_NO_ADMISSIBLE: return "SKMP_E_NO_ADMISSIBLE";
+    case SKMP_E_DUPLICATE_DIM: return "SKMP_E_DUPLICATE_DIM";
+    case SKMP_E_UNKNOWN_DIM: return "SKMP_E_UNKNOWN_DIM";
+    case SKMP_E_LENGTH_MISMATCH: return "SKMP_E_LENGTH_MISMATCH";
+    case SKMP_E_ALL_GROUPS_INERT: return "SKMP_E_ALL_GROUPS_INERT";
+    case SKMP_E_CUDA: return "SKMP_E_CUDA";
+    case SKMP_E_NCCL: return "SKMP_E_NCCL";
+    case SKMP_E_OOM: return "SKMP_E_OOM";
+  }
+  return "SKMP_E_UNKNOWN";
+}
+const char* skmp_last_error(void) { return g_msg.c_str(); }
+int64_t skmp_last_error_index(void) { return g_index; }
+int32_t skmp_abi_version(void) { return SKMP_ABI_VERSION; }
+
+skmp_status sketch_hash_plan(const uint64_t* ids, int64_t d, int32_t k, uint64_t seed,
+                             int32_t* groups, int8_t* signs) {
+  if (d < 0 || k < 1 || (d > 0 && (!ids || !groups || !signs)))
+    return set_error(SKMP_E_INVALID_ARG, "sketch_hash_plan: NULL pointer, d < 0 or k < 1");
+  hash_plan(ids, d, k, seed, groups, signs);
+  return ok();
+}
+
+skmp_status sketch_build(const void* T, int64_t d, int64_t n, int64_t ld, const uint64_t* ids,
+                         const skmp_sketch_cfg* cfg, void* stream, skmp_sketch** out) {
+  if (!T || !ids || !cfg || !out) return set_error(SKMP_E_INVALID_ARG, "sketch_build: NULL argument");
+  if (d < 1 || n < 2 || ld < n || cfg->k < 1)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_build: need d >= 1, n >= 2, ld >= n, k >= 1");
+  if (cfg->dtype != SKMP_F32 && cfg->dtype != SKMP_F64)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_build: bad dtype");
+  if (cfg->proj != SKMP_PROJ_COUNT_SKETCH && cfg->proj != SKMP_PROJ_DENSE)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_build: bad projection kind");
+  if (cfg->proj == SKMP_PROJ_DENSE && !cfg->S)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_build: DENSE needs S (k x d)");
+  if (cfg->signs && !cfg->groups)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_build: explicit signs require explicit groups");
+  if (d > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "sketch_build: d too large");
+  std::vector<int32_t> gg((size_t)d);
+  std::vector<int8_t> ss((size_t)d, 0);
+  std::unordered_map<uint64_t, int64_t> pos;
+  pos.reserve((size_t)d * 2);
+  for (int64_t j = 0; j < d; ++j) {
+    if (!pos.emplace(ids[j], j).second)
+      return set_error(SKMP_E_DUPLICATE_DIM, "sketch_build: duplicate stream id", j);
+  }
+  if (cfg->proj == SKMP_PROJ_COUNT_SKETCH) {
+    hash_plan(ids, d, cfg->k, cfg->seed, gg.data(), ss.data());
+    if (cfg->groups) {
+      for (int64_t j = 0; j < d; ++j) {
+        if (cfg->groups[j] < 0 || cfg->groups[j] >= cfg->k)
+          return set_error(SKMP_E_INVALID_ARG, "sketch_build: explicit group out of range", j);
+        gg[(size_t)j] = cfg->groups[j];
+        if (cfg->signs) {
+          if (cfg->signs[j] != 1 && cfg->signs[j] != -1)
+            return set_error(SKMP_E_INVALID_ARG, "sketch_build: explicit sign must be +1/-1", j);
+          ss[(size_t)j] = cfg->signs[j];
+        }
+      }
+    }
+  } else {
+    std::fill(gg.begin(), gg.end(), -1);
+  }
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  const void* Tdev;
+  int64_t ldd;
+  if ((s = stage_input(T, d, n, ld, cfg->dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
+  StatsHost sh;
+  double *d_mu, *d_inv;
+  if ((s = run_stats(Tdev, d, n, ldd, cfg->dtype, tmp, &sh, &d_mu, &d_inv)) != SKMP_OK) return s;
+
+  skmp_sketch* h = new skmp_sketch();
+  h->dtype = cfg->dtype;
+  h->proj = cfg->proj;
+  h->k = cfg->k;
+  h->n = n;
+  h->seed = cfg->seed;
+  h->st = st;
+  cudaError_t e = cudaMallocAsync((void**)&h->R64, sizeof(double) * (size_t)h->k * n, st);
+  if (e == cudaSuccess && h->dtype == SKMP_F32)
+    e = cudaMallocAsync(&h->R, sizeof(float) * (size_t)h->k * n, st);
+  if (e != cudaSuccess) {
+    sketch_free(h);
+    return cuda_error(e, "sketch_build: allocate R");
+  }
+  if (h->dtype == SKMP_F64) h->R = h->R64;
+  h->ids.assign(ids, ids + d);
+  h->g = gg;
+  h->s = ss;
+  h->mu = sh.mu;
+  h->sigma = sh.sigma;
+  h->pos = std::move(pos);
+  if (h->proj == SKMP_PROJ_DENSE) {
+    h->Scol.resize((size_t)d * h->k);
+    for (int64_t j = 0; j < d; ++j)
+      for (int q = 0; q < h->k; ++q) h->Scol[(size_t)j * h->k + q] = cfg->S[(size_t)q * d + j];
+  }
+  s = project_rows(h, Tdev, ldd, d, h->g, h->s, h->Scol, h->mu, h->sigma, 0, tmp);
+  if (s != SKMP_OK) {
+    sketch_free(h);
+    return s;
+  }
+  *out = h;
+  return ok();
+}
+
+skmp_status sketch_add_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld,
+                           const uint64_t* ids, const double* S_cols, void* stream) {
+  if (!h || !T || !ids) return set_error(SKMP_E_INVALID_ARG, "sketch_add_dim: NULL argument");
+  if (nb < 1 || ld < h->n) return set_error(SKMP_E_INVALID_ARG, "sketch_add_dim: need nb >= 1, ld >= n");
+  if (h->proj == SKMP_PROJ_DENSE && !S_cols)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_add_dim: DENSE needs S_cols (k x nb)");
+  std::unordered_set<uint64_t> seen;
+  for (int64_t j = 0; j < nb; ++j) {
+    if (h->pos.count(ids[j]) || !seen.insert(ids[j]).second)
+      return set_error(SKMP_E_DUPLICATE_DIM, "sketch_add_dim: stream id already present", j);
+  }
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  const void* Tdev;
+  int64_t ldd;
+  if ((s = stage_input(T, nb, h->n, ld, h->dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
+  StatsHost sh;
+  double *d_mu, *d_inv;
+  if ((s = run_stats(Tdev, nb, h->n, ldd, h->dtype, tmp, &sh, &d_mu, &d_inv)) != SKMP_OK) return s;
+  std::vector<int32_t> gg((size_t)nb, -1);
+  std::vector<int8_t> ss((size_t)nb, 0);
+  std::vector<double> Sc;
+  if (h->proj == SKMP_PROJ_COUNT_SKETCH) {
+    hash_plan(ids, nb, h->k, h->seed, gg.data(), ss.data());
+  } else {
+    Sc.resize((size_t)nb * h->k);
+    for (int64_t j = 0; j < nb; ++j)
+      for (int q = 0; q < h->k; ++q) Sc[(size_t)j * h->k + q] = S_cols[(size_t)q * nb + j];
+  }
+  if ((s = project_rows(h, Tdev, ldd, nb, gg, ss, Sc, sh.mu, sh.sigma, +1, tmp)) != SKMP_OK) return s;
+  for (int64_t j = 0; j < nb; ++j) {
+    h->pos[ids[j]] = (int64_t)h->ids.size();
+    h->ids.push_back(ids[j]);
+    h->g.push_back(gg[(size_t)j]);
+    h->s.push_back(ss[(size_t)j]);
+    h->mu.push_back(sh.mu[(size_t)j]);
+    h->sigma.push_back(sh.sigma[(size_t)j]);
+    if (h->proj == SKMP_PROJ_DENSE)
+      h->Scol.insert(h->Scol.end(), Sc.begin() + (size_t)j * h->k, Sc.begin() + (size_t)(j + 1) * h->k);
+  }
+  h->st = st;
+  return ok();
+}
+
+skmp_status sketch_del_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld,
+                           const uint64_t* ids, void* stream) {
+  if (!h || !T || !ids) return set_error(SKMP_E_INVALID_ARG, "sketch_del_dim: NULL argument");
+  if (nb < 1 || ld < h->n) return set_error(SKMP_E_INVALID_ARG, "sketch_del_dim: need nb >= 1, ld >= n");
+  std::vector<int64_t> at((size_t)nb);
+  std::unordered_set<uint64_t> seen;
+  for (int64_t j = 0; j < nb; ++j) {
+    auto it = h->pos.find(ids[j]);
+    if (it == h->pos.end() || !seen.insert(ids[j]).second)
+      return set_error(SKMP_E_UNKNOWN_DIM, "sketch_del_dim: stream id not in the sketch", j);
+    at[(size_t)j] = it->second;
+  }
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  const void* Tdev;
+  int64_t ldd;
+  if ((s = stage_input(T, nb, h->n, ld, h->dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
+  std::vector<int32_t> gg((size_t)nb);
+  std::vector<int8_t> ss((size_t)nb);
+  std::vector<double> mu((size_t)nb), sg((size_t)nb), Sc;
+  for (int64_t j = 0; j < nb; ++j) {
+    const size_t a = (size_t)at[(size_t)j];
+    gg[(size_t)j] = h->g[a];
+    ss[(size_t)j] = h->s[a];
+    mu[(size_t)j] = h->mu[a];   // STORED statistics: add-then-delete is an exact inverse
+    sg[(size_t)j] = h->sigma[a];
+    if (h->proj == SKMP_PROJ_DENSE)
+      Sc.insert(Sc.end(), h->Scol.begin() + a * h->k, h->Scol.begin() + (a + 1) * h->k);
+  }
+  if ((s = project_rows(h, Tdev, ldd, nb, gg, ss, Sc, mu, sg, -1, tmp)) != SKMP_OK) return s;
+  // drop the deleted dims from the plan (keep the remaining input order)
+  std::vector<char> dead(h->ids.size(), 0);
+  for (int64_t a : at) dead[(size_t)a] = 1;
+  size_t w = 0;
+  for (size_t a = 0; a < h->ids.size(); ++a) {
+    if (dead[a]) continue;
+    h->ids[w] = h->ids[a];
+    h->g[w] = h->g[a];
+    h->s[w] = h->s[a];
+    h->mu[w] = h->mu[a];
+    h->sigma[w] = h->sigma[a];
+    if (h->proj == SKMP_PROJ_DENSE)
+      std::copy(h->Scol.begin() + a * h->k, h->Scol.begin() + (a + 1) * h->k, h->Scol.begin() + w * h->k);
+    ++w;
+  }
+  h->ids.resize(w);
+  h->g.resize(w);
+  h->s.resize(w);
+  h->mu.resize(w);
+  h->sigma.resize(w);
+  if (h->proj == SKMP_PROJ_DENSE) h->Scol.resize(w * h->k);
+  h->pos.clear();
+  for (size_t a = 0; a < w; ++a) h->pos[h->ids[a]] = (int64_t)a;
+  h->st = st;
+  return ok();
+}
+
+skmp_status sketch_view(const skmp_sketch* h, const void** R, int32_t* k, int64_t* n, int64_t* d,
+                        int32_t* dtype) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "sketch_view: NULL handle");
+  if (R) *R = h->R;
+  if (k) *k = h->k;
+  if (n) *n = h->n;
+  if (d) *d = (int64_t)h->ids.size();
+  if (dtype) *dtype = h->dtype;
+  return ok();
+}
+
+skmp_status sketch_view64(const skmp_sketch* h, const double** R64) {
+  if (!h || !R64) return set_error(SKMP_E_INVALID_ARG, "sketch_view64: NULL argument");
+  *R64 = h->R64;
+  return ok();
+}
+
+skmp_status sketch_plan(const skmp_sketch* h, uint64_t* ids, int32_t* g, int8_t* s, double* mu,
+                        double* sigma) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "sketch_plan: NULL handle");
+  const size_t d = h->ids.size();
+  if (ids) memcpy(ids, h->ids.data(), d * sizeof(uint64_t));
+  if (g) memcpy(g, h->g.data(), d * sizeof(int32_t));
+  if (s) memcpy(s, h->s.data(), d * sizeof(int8_t));
+  if (mu) memcpy(mu, h->mu.data(), d * sizeof(double));
+  if (sigma) memcpy(sigma, h->sigma.data(), d * sizeof(double));
+  return ok();
+}
+
+void sketch_free(skmp_sketch* h) {
+  if (!h) return;
+  if (h->R && h->R != h->R64) cudaFreeAsync(h->R, h->st);
+  if (h->R64) cudaFreeAsync(h->R64, h->st);
+  delete h;
+}
+
+}  // extern "C"
+
+// ============================================================================================
+// matrix-profile workspace
+// ============================================================================================
+struct skmp_mp {
+  MpDev w;
+  cudaStream_t st = nullptr;
+  std::vector<int32_t> nflat;
+  std::vector<uint8_t> inert;
+  void* base = nullptr;  // single allocation
+};
+
+namespace {
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+skmp_status mp_validate(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                        const skmp_mp_cfg* cfg, int* excl) {
+  if (!R || !cfg) return set_error(SKMP_E_INVALID_ARG, "mp: NULL argument");
+  if (k < 1 || n < 1 || ld < n) return set_error(SKMP_E_INVALID_ARG, "mp: need k >= 1, n >= 1, ld >= n");
+  if (dtype != SKMP_F32 && dtype != SKMP_F64) return set_error(SKMP_E_INVALID_ARG, "mp: bad dtype");
+  if (cfg->m < 2) return set_error(SKMP_E_INVALID_ARG, "mp: m must be >= 2");
+  if (cfg->reseed_rows < 0) return set_error(SKMP_E_INVALID_ARG, "mp: reseed_rows must be >= 0");
+  if (n < cfg->m) return set_error(SKMP_E_SERIES_TOO_SHORT, "mp: n < m");
+  const int64_t n_sub = n - cfg->m + 1;
+  if (n_sub >= (int64_t)INT32_MAX - 1) return set_error(SKMP_E_INVALID_ARG, "mp: n_sub must be < 2^31");
+  *excl = cfg->excl < 0 ? (cfg->m + 1) / 2 : cfg->excl;
+  if (n_sub < 2 * (int64_t)(*excl) + 2)
+    return set_error(SKMP_E_NO_ADMISSIBLE, "mp: n_sub < 2*excl + 2 (some row has no admissible neighbour)");
+  return SKMP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                      const skmp_mp_cfg* cfg, void* stream, skmp_mp** out) {
+  int excl = 0;
+  skmp_status s = mp_validate(R, k, n, ld, dtype, cfg, &excl);
+  if (s) return s;
+  if (!out) return set_error(SKMP_E_INVALID_ARG, "mp_create: NULL out");
+  if ((s = require_device()) != SKMP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  skmp_mp* h = new skmp_mp();
+  MpDev& w = h->w;
+  w.dtype = dtype;
+  w.k = k;
+  w.n = n;
+  w.ld = ld;
+  w.m = cfg->m;
+  w.excl = excl;
+  w.n_sub = n - cfg->m + 1;
+  w.ldq = round_up(w.n_sub + join_pad(dtype), 64);
+  const int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 8192 : 2048);
+  w.L = (int)round_up(L0, 64);
+  w.R = R;
+  const int words = dtype == SKMP_F32 ? 1 : 2;
+  const size_t qsz = dtype == SKMP_F32 ? 16 : 32;
+  const size_t kq = (size_t)k * (size_t)w.ldq;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  const size_t oQ = take(qsz * kq), oMu = take(8 * kq), oSig = take(8 * kq), oFlat = take(kq),
+               oAmax = take(8 * (size_t)k), oNf = take(4 * (size_t)k),
+               oKeys = take(8 * (size_t)words * (size_t)k * (size_t)w.n_sub);
+  cudaError_t e = cudaMallocAsync(&h->base, off, st);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_error(e, "mp_create: allocate workspace");
+  }
+  char* b = static_cast<char*>(h->base);
+  w.Q = b + oQ;
+  w.mu = reinterpret_cast<double*>(b + oMu);
+  w.sig64 = reinterpret_cast<double*>(b + oSig);
+  w.flat = reinterpret_cast<uint8_t*>(b + oFlat);
+  w.amax = reinterpret_cast<double*>(b + oAmax);
+  w.nflat = reinterpret_cast<int32_t*>(b + oNf);
+  w.keys = reinterpret_cast<int64_t*>(b + oKeys);
+  w.flat_list = nullptr;
+  h->st = st;
+  e = launch_mp_prep(w, st);
+  if (e == cudaSuccess) e = launch_keys_init(w, st);
+  h->nflat.assign((size_t)k, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->nflat.data(), w.nflat, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    mp_free(h);
+    return cuda_error(e, "mp_create: window preparation");
+  }
+  h->inert.assign((size_t)k, 0);
+  bool any_flat = false;
+  for (int g = 0; g < k; ++g) {
+    h->inert[(size_t)g] = h->nflat[(size_t)g] == w.n_sub;
+    any_flat |= h->nflat[(size_t)g] > 0;
+  }
+  if (any_flat) {
+    e = cudaMallocAsync((void**)&w.flat_list, sizeof(int32_t) * (size_t)k * (size_t)w.n_sub, st);
+    if (e == cudaSuccess) e = launch_flat_lists(w, h->nflat.data(), st);
+    if (e != cudaSuccess) {
+      mp_free(h);
+      return cuda_error(e, "mp_create: flat lists");
+    }
+  }
+  *out = h;
+  return ok();
+}
+
+skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, int32_t band,
+                    int64_t* diag_lo, int64_t* diag_hi) {
+  if (nbands < 1 || band < 0 || band >= nbands || !diag_lo || !diag_hi || n_sub < 2 || excl < 0)
+    return set_error(SKMP_E_INVALID_ARG, "mp_band: bad arguments");
+  const int64_t W = join_width(dtype);
+  const int64_t lo0 = excl + 1;
+  if (lo0 >= n_sub) {
+    *diag_lo = *diag_hi = 0;
+    return ok();
+  }
+  // cells of diagonals [lo0, x): S(x) = sum_{delta=lo0}^{x-1} (n_sub - delta)
+  auto S = [&](int64_t x) -> double {
+    const double a = (double)(x - lo0);
+    return a * (double)(n_sub - lo0) - a * (a - 1.0) / 2.0;
+  };
+  const double total = S(n_sub);
+  auto edge = [&](int32_t p) -> int64_t {
+    if (p <= 0) return 0;
+    if (p >= nbands) return n_sub;
+    const double target = total * (double)p / (double)nbands;
+    int64_t lo = lo0, hi = n_sub;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (S(mid) < target) lo = mid + 1; else hi = mid;
+    }
+    int64_t x = (lo + W / 2) / W * W;  // nearest multiple of the tile width
+    if (x > n_sub) x = n_sub;
+    return x;
+  };
+  int64_t a = edge(band), b = edge(band + 1);
+  // keep edges monotone after rounding
+  for (int32_t p = band - 1; p >= 0 && a < edge(p); --p) a = edge(p);
+  if (b < a) b = a;
+  *diag_lo = a;
+  *diag_hi = b;
+  return ok();
+}
+
+skmp_status mp_join(skmp_mp* h, int64_t diag_lo, int64_t diag_hi, void* stream) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "mp_join: NULL workspace");
+  if (diag_lo < 0 || diag_hi < 0 || (diag_hi < diag_lo))
+    return set_error(SKMP_E_INVALID_ARG, "mp_join: bad diagonal band");
+  MpDev& w = h->w;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t lo = diag_lo, hi = diag_hi;
+  if (lo == 0 && hi == 0) hi = w.n_sub;
+  if (lo < w.excl + 1) lo = w.excl + 1;
+  if (hi > w.n_sub) hi = w.n_sub;
+  if (lo >= hi) return ok();
+  const int64_t W = join_width(w.dtype);
+  const int64_t blk0 = lo / W, blk1 = (hi + W - 1) / W;
+  const int64_t nblk = blk1 - blk0;
+  std::vector<int64_t> prefix((size_t)nblk + 1, 0);
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t d0 = (blk0 + b) * W;
+    const int64_t dmin = d0 > lo ? d0 : lo;
+    const int64_t rows = w.n_sub - dmin;
+    prefix[(size_t)b + 1] = prefix[(size_t)b] + (rows + w.L - 1) / w.L;
+  }
+  const int64_t ntiles = prefix[(size_t)nblk];
+  if (ntiles > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "mp_join: too many tiles; raise reseed_rows");
+  Temps tmp(st);
+  int64_t* d_prefix = nullptr;
+  skmp_status s = upload(prefix, &d_prefix, tmp);
+  if (s) return s;
+  SKMP_CUDA(launch_mp_join(w, lo, hi, d_prefix, nblk, ntiles, blk0, st));
+  h->st = st;
+  return ok();
+}
+
+skmp_status mp_keys(skmp_mp* h, void** keys, int64_t* count, int32_t* words) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "mp_keys: NULL workspace");
+  const int wd = h->w.dtype == SKMP_F32 ? 1 : 2;
+  if (keys) *keys = h->w.keys;
+  if (count) *count = (int64_t)h->w.k * h->w.n_sub * wd;
+  if (words) *words = wd;
+  return ok();
+}
+
+skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* stream) {
+  if (!h || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize: NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SKMP_CUDA(launch_mp_finalize(h->w, P, I, st));
+  if (inert) memcpy(inert, h->inert.data(), h->inert.size());
+  h->st = st;
+  return ok();
+}
+
+void mp_free(skmp_mp* h) {
+  if (!h) return;
+  if (h->w.flat_list) cudaFreeAsync(h->w.flat_list, h->st);
+  if (h->base) cudaFreeAsync(h->base, h->st);
+  delete h;
+}
+
+skmp_status mp_selfjoin(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                        const skmp_mp_cfg* cfg, void* P, int64_t* I, uint8_t* inert, void* stream) {
+  if (!P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_selfjoin: NULL output");
+  skmp_mp* h = nullptr;
+  skmp_status s = mp_create(R, k, n, ld, dtype, cfg, stream, &h);
+  if (s) return s;
+  s = mp_join(h, 0, 0, stream);
+  if (s == SKMP_OK) s = mp_finalize(h, P, I, inert, stream);
+  mp_free(h);
+  return s;
+}
+
+// ============================================================================================
+// detection
+// ============================================================================================
+skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, int32_t k,
+                         int64_t n_sub, int64_t ldp, int32_t m, int32_t dtype, int32_t top,
+                         int32_t radius, int64_t* t_out, int32_t* g_out, int64_t* nn_out,
+                         double* score_out, int32_t* n_found, void* stream) {
+  if (!P || !I || !t_out || !g_out || !nn_out || !score_out || !n_found)
+    return set_error(SKMP_E_INVALID_ARG, "discord_topk: NULL argument");
+  if (k < 1 || n_sub < 1 || ldp < n_sub || top < 1 || m < 2)
+    return set_error(SKMP_E_INVALID_ARG, "discord_topk: need k >= 1, n_sub >= 1, ldp >= n_sub, top >= 1, m >= 2");
+  if (dtype != SKMP_F32 && dtype != SKMP_F64) return set_error(SKMP_E_INVALID_ARG, "discord_topk: bad dtype");
+  std::vector<uint8_t> hin((size_t)k, 0);
+  int live = 0;
+  for (int g = 0; g < k; ++g) {
+    hin[(size_t)g] = inert ? (inert[g] != 0) : 0;
+    live += !hin[(size_t)g];
+  }
+  if (live == 0) return set_error(SKMP_E_ALL_GROUPS_INERT, "discord_topk: every group is inert");
+  skmp_status s = require_device();
+  if (s) return s;
+  const int rad = radius < 0 ? (m + 1) / 2 : radius;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  uint8_t* d_inert;
+  if ((s = upload(hin, &d_inert, tmp)) != SKMP_OK) return s;
+  double* C;
+  int32_t* G;
+  int64_t* res;
+  int32_t* cnt;
+  char* ws;
+  SKMP_CUDA(tmp.alloc(&C, (size_t)n_sub));
+  SKMP_CUDA(tmp.alloc(&G, (size_t)n_sub));
+  SKMP_CUDA(tmp.alloc(&res, (size_t)top * 4));
+  SKMP_CUDA(tmp.alloc(&cnt, 1));
+  SKMP_CUDA(tmp.alloc(&ws, topk_ws_bytes(n_sub)));
+  SKMP_CUDA(launch_combine(P, ldp, k, n_sub, dtype, d_inert, C, G, st));
+  SKMP_CUDA(launch_topk(C, G, I, ldp, n_sub, top, rad, res, cnt, ws, topk_ws_bytes(n_sub), st));
+  std::vector<int64_t> hres((size_t)top * 4);
+  int32_t hc = 0;
+  SKMP_CUDA(cudaMemcpyAsync(hres.data(), res, sizeof(int64_t) * 4 * top, cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaStreamSynchronize(st));
+  for (int q = 0; q < hc; ++q) {
+    t_out[q] = hres[(size_t)4 * q];
+    g_out[q] = (int32_t)hres[(size_t)4 * q + 1];
+    nn_out[q] = hres[(size_t)4 * q + 2];
+    double v;
+    memcpy(&v, &hres[(size_t)4 * q + 3], sizeof(double));
+    score_out[q] = v;
+  }
+  *n_found = hc;
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Internal declarations shared by the C-ABI layer (api.cu) and the kernel files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sketchmp.h"
+
+namespace skmp {
+
+// ------------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------------
+skmp_status set_error(skmp_status s, const std::string& msg, int64_t index = -1);
+skmp_status cuda_error(cudaError_t e, const char* where);
+
+#define SKMP_CUDA(call)                                            \
+  do {                                                             \
+    cudaError_t e__ = (call);                                      \
+    if (e__ != cudaSuccess) return ::skmp::cuda_error(e__, #call); \
+  } while (0)
+
+#define SKMP_CHECK_LAUNCH(name)                                    \
+  do {                                                             \
+    cudaError_t e__ = cudaGetLastError();                          \
+    if (e__ != cudaSuccess) return ::skmp::cuda_error(e__, name);  \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// constants shared by host and device code
+// ------------------------------------------------------------------------------------------
+constexpr double kFlatEps = 1e-12;  // readings 4/5
+
+// Join geometry (see mp_join.cu).  The tile width W = NT*D diagonals is also the band
+// rounding unit of mp_band; rows per chunk C; a tile spans `reseed_rows` rows.
+constexpr int kJoinNT = 128;
+constexpr int kJoinD32 = 8;
+constexpr int kJoinD64 = 8;
+constexpr int kJoinC = 32;
+inline int join_width(int dtype) { return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : kJoinD32); }
+// padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
+inline int64_t join_pad(int dtype) { return join_width(dtype) + 4 * kJoinC + 64; }
+
+// ------------------------------------------------------------------------------------------
+// stream-statistics (K1) and projection (K2/K2d/K3) launchers — sketch.cu
+// ------------------------------------------------------------------------------------------
+struct StatsOut {  // device arrays of length d
+  double* mu;
+  double* sigma;
+  double* inv;     // 1/sigma
+  int32_t* flag;   // 0 ok, 1 nonfinite, 2 constant
+};
+// Computes per-row stats of T (d x ld) over n samples.  ws must hold stats_ws_bytes(d, n).
+size_t stats_ws_bytes(int64_t d, int64_t n);
+cudaError_t launch_stream_stats(const void* T, int64_t d, int64_t n, int64_t ld, int dtype,
+                                StatsOut out, void* ws, cudaStream_t st);
+
+// Count sketch projection: for each group g, R64[g,:] (+)= sum over list entries e in
+// [off[g], off[g+1]) of sign[e] * ((T[row[e], :] - mu[e]) * inv[e]).  `mode`: 0 = overwrite
+// (build), +1 = add into R64, -1 = subtract from R64.  Then R = dtype(R64) when R != R64.
+struct CsrPlan {
+  const int32_t* off;    // k+1
+  const int32_t* row;    // rows of T
+  const double* mu;      // per entry
+  const double* inv;     // per entry
+  const int8_t* sign;    // per entry
+};
+cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype, int k,
+                                 CsrPlan plan, int mode, double* R64, void* R, cudaStream_t st);
+// Dense projection: R64[g,:] (+)= sum_j S[g*ldS + j] * ((T[j,:] - mu[j]) * inv[j]).
+cudaError_t launch_project_dense(const void* T, int64_t ld, int64_t n, int dtype, int k,
+                                 int64_t nstreams, const double* S, int64_t ldS, const double* mu,
+                                 const double* inv, int mode, double* R64, void* R,
+                                 cudaStream_t st);
+
+// ------------------------------------------------------------------------------------------
+// matrix profile (K4-K7) — mp_prep.cu, mp_join.cu, mp_final.cu
+// ------------------------------------------------------------------------------------------
+struct MpDev {
+  int dtype;
+  int k;
+  int64_t n, ld, n_sub, ldq;  // ldq: stride (windows) of the prepared arrays per series
+  int m, excl, L;             // L = reseed rows (tile height)
+  const void* R;              // k x ld (dtype)
+  void* Q;                    // k x ldq x {df, dg, inv, 0} (dtype)
+  double* mu;                 // k x ldq
+  double* sig64;              // k x ldq  window population std (FP64)
+  uint8_t* flat;              // k x ldq
+  double* amax;               // k
+  int32_t* nflat;             // k
+  int64_t* keys;              // k x n_sub x words
+  int32_t* flat_list;         // k x n_sub (only filled for series with nflat > 0)
+};
+cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st);
+cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
+// band join: tiles described by blocks of W diagonals [dlo, dhi)
+cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
+                           int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
+cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);
+cudaError_t launch_mp_finalize(const MpDev& w, void* P, int64_t* I, cudaStream_t st);
+
+// ------------------------------------------------------------------------------------------
+// detection (K8) — detect.cu
+// ------------------------------------------------------------------------------------------
+cudaError_t launch_combine(const void* P, int64_t ldp, int k, int64_t n_sub, int dtype,
+                           const uint8_t* d_inert, double* C, int32_t* G, cudaStream_t st);
+// top-K greedy over C (double, n_sub); result rows (t, g, nn, score) into d_res (int64 x 4 per
+// entry, score bit-cast), count into d_count.
+cudaError_t launch_topk(double* C, const int32_t* G, const int64_t* I, int64_t ldi, int64_t n_sub,
+                        int top, int radius, int64_t* d_res, int32_t* d_count, void* ws,
+                        size_t ws_bytes, cudaStream_t st);
+size_t topk_ws_bytes(int64_t n_sub);
+
+// host hash (hash.cpp)
+void cw_params(uint64_t seed, uint64_t* a, uint64_t* b, uint64_t* c, uint64_t* e);
+void hash_plan(const uint64_t* ids, int64_t d, int32_t k, uint64_t seed, int32_t* g, int8_t* s);
+
+}  // namespace skmp

@@ -1,0 +1,212 @@
+// K4: per-window statistics and recurrence terms for the matrix-profile self-join.
+//
+// Def. 3: dist is the z-normalised Euclidean distance between windows
+// T_{i,m} (Def. 2).  With mu_i, sigma_i the window mean / population std and
+// cov(i,j) = sum_{t<m} (R[i+t]-mu_i)(R[j+t]-mu_j):
+//     dist(i,j)^2 = 2m (1 - rho_ij),  rho_ij = cov(i,j) / (m sigma_i sigma_j)
+// and along a diagonal (the STOMP/SCAMP "QT" recurrence, north_star):
+//     cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i,
+//     df_i = (R[i+m-1] - R[i-1]) / 2,   dg_i = (R[i+m-1] - mu_i) + (R[i-1] - mu_{i-1}).
+// mu_i and sigma_i are computed here in FP64 by DIRECT per-window sums (never global prefix
+// sums: SURVEY E5 measured 2e-7 rho drift from prefix-sum means even in FP64).  Flat windows
+// (sigma_i <= 1e-12 (max|R_g|+1), reading 5) get inv = 0.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace skmp {
+namespace {
+
+template <typename T>
+__global__ void amax_kernel(const T* __restrict__ R, int64_t ld, int64_t n, double* amax) {
+  const int g = blockIdx.y;
+  const T* r = R + (int64_t)g * ld;
+  double a = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    a = fmax(a, fabs((double)r[t]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+  if ((threadIdx.x & 31) == 0) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(amax + g),
+              (unsigned long long)__double_as_longlong(a));
+  }
+}
+
+constexpr int kPrepThreads = 256;
+
+template <typename T> struct Q4;
+template <> struct Q4<float> { using type = float4; };
+struct __align__(32) double4a { double x, y, z, w; };
+template <> struct Q4<double> { using type = double4a; };
+
+template <typename T>
+__global__ void __launch_bounds__(kPrepThreads)
+prep_kernel(MpDev w) {
+  extern __shared__ double xs[];  // R[i0-1 .. i0+kPrepThreads+m-1)
+  using QT = typename Q4<T>::type;
+  const int g = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * kPrepThreads;
+  const int m = w.m;
+  const T* r = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
+  const int span = kPrepThreads + m;
+  for (int s = threadIdx.x; s < span; s += kPrepThreads) {
+    const int64_t t = i0 - 1 + s;
+    xs[s] = (t >= 0 && t < w.n) ? (double)r[t] : 0.0;
+  }
+  __syncthreads();
+  const int64_t i = i0 + threadIdx.x;
+  if (i >= w.n_sub) return;
+  const double* x = xs + 1 + threadIdx.x;  // x[s] = R[i+s]; x[-1] = R[i-1]
+  // mean of window i and of window i-1, same sequential order as each other's owner thread
+  double s1 = 0.0;
+  for (int s = 0; s < m; ++s) s1 += x[s];
+  const double mu = s1 / m;
+  double q = 0.0;
+  for (int s = 0; s < m; ++s) {
+    const double c = x[s] - mu;
+    q = __dadd_rn(q, __dmul_rn(c, c));  // no contraction: same rounding as the plain definition
+  }
+  const double sig = sqrt(q / m);
+  const bool flat = !(sig > kFlatEps * (w.amax[g] + 1.0));
+  double df = 0.0, dg = 0.0;
+  if (i > 0) {
+    double s0 = 0.0;
+    for (int s = -1; s < m - 1; ++s) s0 += x[s];
+    const double mu_prev = s0 / m;
+    df = (x[m - 1] - x[-1]) * 0.5;
+    dg = (x[m - 1] - mu) + (x[-1] - mu_prev);
+  }
+  const double invm = flat ? 0.0 : 1.0 / (sqrt((double)m) * sig);
+  QT qv;
+  qv.x = (T)df;
+  qv.y = (T)dg;
+  qv.z = (T)invm;
+  qv.w = (T)0;
+  const int64_t o = (int64_t)g * w.ldq + i;
+  reinterpret_cast<QT*>(w.Q)[o] = qv;
+  w.mu[o] = mu;
+  w.sig64[o] = sig;
+  w.flat[o] = flat ? 1 : 0;
+  // one atomic per warp: the lowest active lane adds the warp's flat count
+  const unsigned act = __activemask();
+  const unsigned fl = __ballot_sync(act, flat);
+  if ((int)(threadIdx.x & 31) == __ffs(act) - 1 && fl) atomicAdd(w.nflat + g, __popc(fl));
+}
+
+__global__ void keys_init_kernel(int64_t* keys, int64_t count, int words) {
+  // FP32 key: (orderable(-inf) << 32) | 0;  FP64 key: {orderable64(-inf), INT64_MIN}
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  if (words == 1) {
+    keys[i] = (int64_t)(((uint64_t)(uint32_t)0x807FFFFFu) << 32);
+  } else {
+    keys[2 * i] = (int64_t)0x800FFFFFFFFFFFFFull;
+    keys[2 * i + 1] = INT64_MIN;
+  }
+}
+
+// Ordered compaction of the flat-window indices of one series (single CTA; launched only for
+// series that have flat windows, which is rare).
+__global__ void flat_list_kernel(const uint8_t* __restrict__ flat, int64_t ldq, int64_t n_sub,
+                                 int32_t* __restrict__ list, const int32_t* __restrict__ series) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t base_sh;
+  const int g = series[blockIdx.x];
+  const uint8_t* f = flat + (int64_t)g * ldq;
+  int32_t* out = list + (int64_t)g * n_sub;
+  if (threadIdx.x == 0) base_sh = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = 0; c0 < n_sub; c0 += blockDim.x) {
+    const int64_t i = c0 + threadIdx.x;
+    const bool p = i < n_sub && f[i];
+    const unsigned b = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) wsum[wid] = __popc(b);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int q = 0; q < nw; ++q) {
+      if (q < wid) before += wsum[q];
+      total += wsum[q];
+    }
+    const int base = base_sh;
+    if (p) out[base + before + __popc(b & ((1u << lane) - 1))] = (int32_t)i;
+    __syncthreads();
+    if (threadIdx.x == 0) base_sh = base + total;
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(w.amax, 0, sizeof(double) * w.k, st);
+  if (e) return e;
+  e = cudaMemsetAsync(w.nflat, 0, sizeof(int32_t) * w.k, st);
+  if (e) return e;
+  const size_t qsz = (w.dtype == SKMP_F32 ? 16 : 32);
+  e = cudaMemsetAsync(w.Q, 0, qsz * (size_t)w.k * (size_t)w.ldq, st);
+  if (e) return e;
+  {
+    const int64_t blocks = (w.n + 255) / 256;
+    dim3 grid((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)w.k);
+    if (w.dtype == SKMP_F32)
+      amax_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w.R), w.ld, w.n, w.amax);
+    else
+      amax_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(w.R), w.ld, w.n, w.amax);
+    e = cudaGetLastError();
+    if (e) return e;
+  }
+  dim3 grid((unsigned)((w.n_sub + kPrepThreads - 1) / kPrepThreads), (unsigned)w.k);
+  const size_t smem = sizeof(double) * (kPrepThreads + w.m);
+  if (w.dtype == SKMP_F32) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(prep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+    }
+    prep_kernel<float><<<grid, kPrepThreads, smem, st>>>(w);
+  } else {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(prep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e) return e;
+    }
+    prep_kernel<double><<<grid, kPrepThreads, smem, st>>>(w);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st) {
+  const int words = w.dtype == SKMP_F32 ? 1 : 2;
+  const int64_t count = (int64_t)w.k * w.n_sub;
+  keys_init_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(w.keys, count, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st) {
+  // simple and robust: one small device array of series ids
+  int nser = 0;
+  for (int g = 0; g < w.k; ++g) nser += h_nflat[g] > 0;
+  if (nser == 0) return cudaSuccess;
+  int32_t* d_ids = nullptr;
+  cudaError_t e = cudaMallocAsync(&d_ids, sizeof(int32_t) * nser, st);
+  if (e) return e;
+  int32_t* h_ids = nullptr;
+  e = cudaMallocHost(&h_ids, sizeof(int32_t) * nser);
+  if (e) return e;
+  int q = 0;
+  for (int g = 0; g < w.k; ++g)
+    if (h_nflat[g] > 0) h_ids[q++] = g;
+  e = cudaMemcpyAsync(d_ids, h_ids, sizeof(int32_t) * nser, cudaMemcpyHostToDevice, st);
+  if (e) return e;
+  flat_list_kernel<<<nser, 1024, 0, st>>>(w.flat, w.ldq, w.n_sub, w.flat_list, d_ids);
+  e = cudaGetLastError();
+  if (e) return e;
+  e = cudaStreamSynchronize(st);  // h_ids must outlive the copy
+  cudaFreeHost(h_ids);
+  if (e) return e;
+  return cudaFreeAsync(d_ids, st);
+}
+
+}  // namespace skmp

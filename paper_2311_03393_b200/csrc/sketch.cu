@@ -1,0 +1,431 @@
+// Sketch kernels (K1 stream statistics, K2 count-sketch projection, K2d dense projection,
+// K3 add/delete as K2 in accumulate mode).
+//
+// PAPER.md §3.1 Alg. 1: R^(g) = sum_{j in J_g} s(j) T_bar^(j), "basically just
+// reading the input"; T_bar is the z-normalised input (reading 3: each stream's
+// own mean and population std).  §3.3: the sketch is linear, so adding/deleting a
+// dimension is R^(h(j)) +/- s(j) T_bar^(j).
+//
+// Both kernels are HBM-bound streaming passes over the d x n input: K1 reads T once to get
+// (mu_j, 1/sigma_j), K2 reads it again and writes R.  Accumulation is FP64 in ascending input
+// order inside each group with explicit _rn intrinsics (no FMA contraction), rounded once to
+// the output dtype (reading 14).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace skmp {
+
+namespace {
+
+constexpr int kStatsThreads = 256;
+constexpr int kStatsPerThread = 16;
+constexpr int kStatsChunk = kStatsThreads * kStatsPerThread;  // 4096 samples per block
+
+struct Partial {
+  double cnt, mean, m2, amax;
+};
+
+template <typename T>
+__device__ __forceinline__ void load_chunk(const T* __restrict__ x, int64_t base, int64_t n,
+                                           double (&v)[kStatsPerThread], int& cnt, bool vec);
+
+template <>
+__device__ __forceinline__ void load_chunk<float>(const float* __restrict__ x, int64_t base,
+                                                  int64_t n, double (&v)[kStatsPerThread],
+                                                  int& cnt, bool vec) {
+  // layout: element (it*256 + tid)*4 + q of the chunk, it = 0..3, q = 0..3 (coalesced float4)
+  cnt = 0;
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    int64_t e = base + ((int64_t)it * kStatsThreads + threadIdx.x) * 4;
+    if (vec && e + 4 <= n) {
+      float4 f = __ldcs(reinterpret_cast<const float4*>(x + e));
+      v[it * 4 + 0] = f.x; v[it * 4 + 1] = f.y; v[it * 4 + 2] = f.z; v[it * 4 + 3] = f.w;
+      cnt += 4;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (e + q < n) { v[it * 4 + q] = x[e + q]; ++cnt; } else { v[it * 4 + q] = 0.0; }
+      }
+    }
+  }
+}
+
+template <>
+__device__ __forceinline__ void load_chunk<double>(const double* __restrict__ x, int64_t base,
+                                                   int64_t n, double (&v)[kStatsPerThread],
+                                                   int& cnt, bool vec) {
+  cnt = 0;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    int64_t e = base + ((int64_t)it * kStatsThreads + threadIdx.x) * 2;
+    if (vec && e + 2 <= n) {
+      double2 f = __ldcs(reinterpret_cast<const double2*>(x + e));
+      v[it * 2 + 0] = f.x; v[it * 2 + 1] = f.y;
+      cnt += 2;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (e + q < n) { v[it * 2 + q] = x[e + q]; ++cnt; } else { v[it * 2 + q] = 0.0; }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double block_sum(double x, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = x;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kStatsThreads / 32; ++i) t += sh[i];  // fixed order: deterministic
+  return t;
+}
+
+__device__ __forceinline__ double block_max(double x, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = x;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kStatsThreads / 32; ++i) t = fmax(t, sh[i]);
+  return t;
+}
+
+// K1a: per (stream, chunk) count, mean, M2 (two passes over registers), max|x|, finiteness.
+template <typename T>
+__global__ void __launch_bounds__(kStatsThreads)
+stats_partial_kernel(const T* __restrict__ Tm, int64_t n, int64_t ld, int64_t nchunks,
+                     Partial* __restrict__ part, int32_t* __restrict__ flag, bool vec) {
+  __shared__ double sh[kStatsThreads / 32];
+  const int64_t j = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  const T* x = Tm + j * ld;
+  const int64_t base = c * kStatsChunk;
+  double v[kStatsPerThread];
+  int cnt;
+  load_chunk<T>(x, base, n, v, cnt, vec);
+  const int64_t total = min((int64_t)kStatsChunk, n - base);
+  double s = 0.0, a = 0.0;
+  bool finite = true;
+#pragma unroll
+  for (int q = 0; q < kStatsPerThread; ++q) {
+    s += v[q];
+    a = fmax(a, fabs(v[q]));
+    finite &= isfinite(v[q]);
+  }
+  // non-finite inputs poison the sums; flag them (the host reports NONFINITE)
+  if (!finite) atomicMax(flag + j, 1);
+  s = block_sum(s, sh);
+  const double mean = s / (double)total;
+  constexpr int VN = (sizeof(T) == 4) ? 4 : 2;
+  double q2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < kStatsPerThread; ++q) {
+    const int64_t e = base + ((int64_t)(q / VN) * kStatsThreads + threadIdx.x) * VN + (q % VN);
+    const double dlt = (e < n) ? v[q] - mean : 0.0;  // padding slots contribute nothing
+    q2 += dlt * dlt;
+  }
+  (void)cnt;
+  q2 = block_sum(q2, sh);
+  a = block_max(a, sh);
+  if (threadIdx.x == 0) {
+    Partial p;
+    p.cnt = (double)total;
+    p.mean = mean;
+    p.m2 = fmax(q2, 0.0);
+    p.amax = a;
+    part[j * nchunks + c] = p;
+  }
+}
+
+// K1b: per stream, Chan's pairwise combine of the chunk partials in chunk order.
+__global__ void stats_combine_kernel(const Partial* __restrict__ part, int64_t d, int64_t nchunks,
+                                     StatsOut out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  const Partial* p = part + j * nchunks;
+  double na = p[0].cnt, mean = p[0].mean, m2 = p[0].m2, amax = p[0].amax;
+  for (int64_t c = 1; c < nchunks; ++c) {
+    const double nb = p[c].cnt;
+    const double delta = p[c].mean - mean;
+    const double nn = na + nb;
+    mean += delta * (nb / nn);
+    m2 += p[c].m2 + delta * delta * (na * nb / nn);
+    amax = fmax(amax, p[c].amax);
+    na = nn;
+  }
+  const double sigma = sqrt(m2 / na);
+  out.mu[j] = mean;
+  out.sigma[j] = sigma;
+  int f = out.flag[j];
+  if (f == 0 && !(sigma > kFlatEps * (amax + 1.0))) f = 2;  // reading 4: constant stream
+  if (f == 0 && !isfinite(sigma)) f = 1;
+  out.flag[j] = f;
+  out.inv[j] = f == 0 ? 1.0 / sigma : 0.0;
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: count-sketch projection.  Block = (time tile, group g).  Each thread owns kVec*kIt
+// consecutive-by-vector samples; the group's entry list is staged in shared memory in batches;
+// four entries are in flight per step for memory-level parallelism.
+// ------------------------------------------------------------------------------------------
+constexpr int kProjThreads = 256;
+constexpr int kProjBatch = 256;
+
+template <typename T> struct VecOf;
+template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
+template <> struct VecOf<double> { using V = double2; static constexpr int N = 2; };
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, double* out, int64_t e, int64_t n, bool vec);
+template <>
+__device__ __forceinline__ void vload<float>(const float* p, double* out, int64_t e, int64_t n,
+                                             bool vec) {
+  if (vec && e + 4 <= n) {
+    float4 f = __ldcs(reinterpret_cast<const float4*>(p + e));
+    out[0] = f.x; out[1] = f.y; out[2] = f.z; out[3] = f.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = (e + q < n) ? (double)p[e + q] : 0.0;
+  }
+}
+template <>
+__device__ __forceinline__ void vload<double>(const double* p, double* out, int64_t e, int64_t n,
+                                              bool vec) {
+  if (vec && e + 2 <= n) {
+    double2 f = __ldcs(reinterpret_cast<const double2*>(p + e));
+    out[0] = f.x; out[1] = f.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) out[q] = (e + q < n) ? p[e + q] : 0.0;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_out(T* R, int64_t e, int64_t n, const double* v);
+template <>
+__device__ __forceinline__ void store_out<float>(float* R, int64_t e, int64_t n, const double* v) {
+  if (e + 4 <= n && ((reinterpret_cast<uintptr_t>(R + e) & 15) == 0)) {
+    *reinterpret_cast<float4*>(R + e) = make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+  } else {
+    for (int q = 0; q < 4; ++q) if (e + q < n) R[e + q] = (float)v[q];
+  }
+}
+template <>
+__device__ __forceinline__ void store_out<double>(double* R, int64_t e, int64_t n, const double* v) {
+  if (e + 2 <= n && ((reinterpret_cast<uintptr_t>(R + e) & 15) == 0)) {
+    *reinterpret_cast<double2*>(R + e) = make_double2(v[0], v[1]);
+  } else {
+    for (int q = 0; q < 2; ++q) if (e + q < n) R[e + q] = v[q];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kProjThreads)
+project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan plan, int mode,
+                     double* __restrict__ R64, T* __restrict__ R, bool vec) {
+  constexpr int VN = VecOf<T>::N;
+  constexpr int IT = (sizeof(T) == 4) ? 2 : 4;  // vectors per thread: 8 floats or 8 doubles
+  constexpr int E = VN * IT;                    // samples per thread
+  __shared__ int32_t s_row[kProjBatch];
+  __shared__ double s_mu[kProjBatch];
+  __shared__ double s_inv[kProjBatch];
+  __shared__ int8_t s_sign[kProjBatch];
+
+  const int g = blockIdx.y;
+  const int32_t e0 = plan.off[g], e1 = plan.off[g + 1];
+  if (mode != 0 && e0 == e1) return;  // update of an untouched group: nothing to do
+  const int64_t tile = (int64_t)kProjThreads * E;
+  const int64_t base = (int64_t)blockIdx.x * tile;
+
+  double acc[E];
+  double* r64 = R64 + (int64_t)g * n;
+  if (mode == 0) {
+#pragma unroll
+    for (int q = 0; q < E; ++q) acc[q] = 0.0;
+  } else {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
+#pragma unroll
+      for (int q = 0; q < VN; ++q) acc[it * VN + q] = (e + q < n) ? r64[e + q] : 0.0;
+    }
+  }
+
+  for (int32_t b0 = e0; b0 < e1; b0 += kProjBatch) {
+    const int nb = min(kProjBatch, e1 - b0);
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      s_row[threadIdx.x] = plan.row[b0 + threadIdx.x];
+      s_mu[threadIdx.x] = plan.mu[b0 + threadIdx.x];
+      s_inv[threadIdx.x] = plan.inv[b0 + threadIdx.x];
+      s_sign[threadIdx.x] = plan.sign[b0 + threadIdx.x];
+    }
+    __syncthreads();
+    int q0 = 0;
+    constexpr int U = 4;
+    for (; q0 + U <= nb; q0 += U) {
+      double x[U][E];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const T* row = Tm + (int64_t)s_row[q0 + u] * ld;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
+          vload<T>(row, &x[u][it * VN], e, n, vec);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double mu = s_mu[q0 + u], inv = s_inv[q0 + u];
+        const bool pos = (s_sign[q0 + u] > 0) == (mode >= 0);
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+          const double z = __dmul_rn(__dsub_rn(x[u][q], mu), inv);
+          acc[q] = pos ? __dadd_rn(acc[q], z) : __dsub_rn(acc[q], z);
+        }
+      }
+    }
+    for (; q0 < nb; ++q0) {
+      double x[E];
+      const T* row = Tm + (int64_t)s_row[q0] * ld;
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
+        vload<T>(row, &x[it * VN], e, n, vec);
+      }
+      const double mu = s_mu[q0], inv = s_inv[q0];
+      const bool pos = (s_sign[q0] > 0) == (mode >= 0);
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const double z = __dmul_rn(__dsub_rn(x[q], mu), inv);
+        acc[q] = pos ? __dadd_rn(acc[q], z) : __dsub_rn(acc[q], z);
+      }
+    }
+  }
+
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
+#pragma unroll
+    for (int h2 = 0; h2 < VN; h2 += 2)  // FP64 master: VN input samples as double2 stores
+      store_out<double>(r64, e + h2, n, &acc[it * VN + h2]);
+    if ((void*)R != (void*)R64) store_out<T>(R + (int64_t)g * n, e, n, &acc[it * VN]);
+  }
+}
+
+// K2d: dense projection, 8 groups per block, one sample per thread (small configs only).
+constexpr int kDenseG = 8;
+template <typename T>
+__global__ void project_dense_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, int k,
+                                     int64_t nstreams, const double* __restrict__ S, int64_t ldS,
+                                     const double* __restrict__ mu, const double* __restrict__ inv,
+                                     int mode, double* __restrict__ R64, T* __restrict__ R) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g0 = blockIdx.y * kDenseG;
+  if (t >= n) return;
+  double acc[kDenseG];
+#pragma unroll
+  for (int q = 0; q < kDenseG; ++q)
+    acc[q] = (mode != 0 && g0 + q < k) ? R64[(int64_t)(g0 + q) * n + t] : 0.0;
+  for (int64_t j = 0; j < nstreams; ++j) {
+    const double z = __dmul_rn(__dsub_rn((double)Tm[j * ld + t], mu[j]), inv[j]);
+#pragma unroll
+    for (int q = 0; q < kDenseG; ++q) {
+      if (g0 + q < k) {
+        const double c = __dmul_rn(S[(int64_t)(g0 + q) * ldS + j], z);
+        acc[q] = mode >= 0 ? __dadd_rn(acc[q], c) : __dsub_rn(acc[q], c);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kDenseG; ++q) {
+    if (g0 + q < k) {
+      R64[(int64_t)(g0 + q) * n + t] = acc[q];
+      if ((void*)R != (void*)R64) R[(int64_t)(g0 + q) * n + t] = (T)acc[q];
+    }
+  }
+}
+
+}  // namespace
+
+size_t stats_ws_bytes(int64_t d, int64_t n) {
+  const int64_t nchunks = (n + kStatsChunk - 1) / kStatsChunk;
+  return sizeof(Partial) * (size_t)(d * nchunks);
+}
+
+cudaError_t launch_stream_stats(const void* T, int64_t d, int64_t n, int64_t ld, int dtype,
+                                StatsOut out, void* ws, cudaStream_t st) {
+  const int64_t nchunks = (n + kStatsChunk - 1) / kStatsChunk;
+  cudaError_t e = cudaMemsetAsync(out.flag, 0, sizeof(int32_t) * d, st);
+  if (e != cudaSuccess) return e;
+  int64_t left = d;
+  int64_t off = 0;
+  while (left > 0) {  // grid.y <= 65535
+    const int64_t dd = left < 65535 ? left : 65535;
+    dim3 grid((unsigned)nchunks, (unsigned)dd);
+    if (dtype == SKMP_F32) {
+      const float* p = static_cast<const float*>(T) + off * ld;
+      const bool vec = ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (ld % 4 == 0);
+      stats_partial_kernel<float><<<grid, kStatsThreads, 0, st>>>(
+          p, n, ld, nchunks, static_cast<Partial*>(ws) + off * nchunks, out.flag + off, vec);
+    } else {
+      const double* p = static_cast<const double*>(T) + off * ld;
+      const bool vec = ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (ld % 2 == 0);
+      stats_partial_kernel<double><<<grid, kStatsThreads, 0, st>>>(
+          p, n, ld, nchunks, static_cast<Partial*>(ws) + off * nchunks, out.flag + off, vec);
+    }
+    left -= dd;
+    off += dd;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  stats_combine_kernel<<<(unsigned)((d + 127) / 128), 128, 0, st>>>(static_cast<Partial*>(ws), d,
+                                                                   nchunks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype, int k,
+                                 CsrPlan plan, int mode, double* R64, void* R, cudaStream_t st) {
+  if (dtype == SKMP_F32) {
+    const int64_t tile = (int64_t)kProjThreads * 8;
+    dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
+    const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 4 == 0);
+    project_count_kernel<float><<<grid, kProjThreads, 0, st>>>(
+        static_cast<const float*>(T), ld, n, plan, mode, R64, static_cast<float*>(R), vec);
+  } else {
+    const int64_t tile = (int64_t)kProjThreads * 8;
+    dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
+    const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 2 == 0);
+    project_count_kernel<double><<<grid, kProjThreads, 0, st>>>(
+        static_cast<const double*>(T), ld, n, plan, mode, R64, static_cast<double*>(R), vec);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project_dense(const void* T, int64_t ld, int64_t n, int dtype, int k,
+                                 int64_t nstreams, const double* S, int64_t ldS, const double* mu,
+                                 const double* inv, int mode, double* R64, void* R,
+                                 cudaStream_t st) {
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)((k + kDenseG - 1) / kDenseG));
+  if (dtype == SKMP_F32)
+    project_dense_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(T), ld, n, k,
+                                                      nstreams, S, ldS, mu, inv, mode, R64,
+                                                      static_cast<float*>(R));
+  else
+    project_dense_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(T), ld, n, k,
+                                                       nstreams, S, ldS, mu, inv, mode, R64,
+                                                       static_cast<double*>(R));
+  return cudaGetLastError();
+}
+
+}  // namespace skmp

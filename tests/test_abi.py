@@ -1,0 +1,86 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every function include/sketchmp.h
+declares, and its host-only entry points (hash plan, band partition, errors) work without a
+GPU; compute entry points fail loudly (no CPU fallback)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2311_03393_b200 as skmp
+from oracle.hashplan import plan_count_sketch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "sketchmp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(?:skmp_status|void|const char\*|int64_t|int32_t)\s+\**(\w+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    L = skmp.lib()
+    names = _declared()
+    assert len(names) >= 20, names
+    for n in names:
+        assert hasattr(L, n), f"missing export {n}"
+    assert set(names) >= set(skmp._SIGS), set(skmp._SIGS) - set(names)
+    assert L.skmp_abi_version() == 1
+
+
+def test_status_strings():
+    L = skmp.lib()
+    for code, name in skmp.STATUS.items():
+        assert L.skmp_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("k,seed", [(1, 0), (7, 2311033932), (64, 12345), (100, 2**63 + 5)])
+def test_hash_plan_matches_oracle(k, seed):
+    """C++ Carter-Wegman plan (128-bit products) == the oracle's Python-integer plan, bit-equal."""
+    ids = np.concatenate([np.arange(0, 3000), np.array([2**61 - 2, 2**61 - 1, 2**61, 2**64 - 1], dtype=np.uint64)]).astype(np.uint64)
+    g, s = skmp.sketch_hash_plan(ids, k, seed)
+    go, so = plan_count_sketch([int(x) for x in ids], k, seed)
+    assert np.array_equal(g, np.array(go, dtype=np.int32))
+    assert np.array_equal(s, np.array(so, dtype=np.int8))
+
+
+def test_hash_plan_invalid():
+    with pytest.raises(skmp.SkmpError) as e:
+        skmp.sketch_hash_plan(np.arange(3), 0, 1)
+    assert e.value.name == "SKMP_E_INVALID_ARG"
+
+
+@pytest.mark.parametrize("n_sub,excl,dtype", [(1999745, 128, 0), (199745, 128, 0), (19901, 50, 1), (1951, 25, 1)])
+def test_band_partition(n_sub, excl, dtype):
+    W = 128 * 8
+    for nb in (1, 2, 4, 8):
+        edges = []
+        for b in range(nb):
+            lo, hi = skmp.mp_band(n_sub, excl, dtype, nb, b)
+            edges.append((lo, hi))
+        # contiguous cover of [0, n_sub), interior edges on the tile grid
+        assert edges[0][0] == 0 and edges[-1][1] == n_sub
+        for (a, b_), (c, d) in zip(edges, edges[1:]):
+            assert b_ == c and c % W == 0 and a <= b_
+        # balance: each band within one tile-width of cells of the ideal share
+        lo0 = excl + 1
+        cells = lambda a, b: sum(max(0, n_sub - x) for x in range(max(a, lo0), b)) if n_sub < 10**5 else \
+            (lambda A, B: (B - A) * n_sub - (B * (B - 1) - A * (A - 1)) // 2)(max(a, lo0), max(b, lo0))
+        tot = cells(0, n_sub)
+        for a, b in edges:
+            assert abs(cells(a, b) - tot / nb) <= W * n_sub + 1
+
+
+def test_compute_calls_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    T = np.random.default_rng(0).standard_normal((3, 100))
+    with pytest.raises(skmp.SkmpError) as e:
+        skmp.sketch_build(T, np.arange(3), 2, seed=1)
+    assert e.value.name == "SKMP_E_CUDA"
