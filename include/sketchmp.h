@@ -58,6 +58,8 @@ const char* skmp_status_string(skmp_status s);   /* static string               
 const char* skmp_last_error(void);               /* thread-local text of the last non-OK call  */
 int64_t skmp_last_error_index(void);             /* offending stream/group/row, or -1          */
 int32_t skmp_abi_version(void);                  /* SKMP_ABI_VERSION                           */
+int64_t skmp_launch_count(void);                 /* kernels this library launched so far (all  */
+                                                 /* threads); bench.py reports the delta       */
 
 /* ---------------------------------------------------------------------------------------------
  * Hash plan (host-only; callable without a GPU).  The count-sketch pair (h, s) of P:L200-204
@@ -125,6 +127,9 @@ skmp_status sketch_view64(const skmp_sketch* h, const double** R64);
  * mu, sigma (sign is 0 and group -1 for DENSE). */
 skmp_status sketch_plan(const skmp_sketch* h, uint64_t* ids, int32_t* g, int8_t* s, double* mu,
                         double* sigma);
+/* Re-round R = dtype(R64) after R64 was modified outside the library (e.g. a cross-GPU
+ * sum-allreduce of per-rank partial sketches).  Asynchronous. */
+skmp_status sketch_refresh(skmp_sketch* h, void* stream);
 void sketch_free(skmp_sketch* h);
 
 /* ---------------------------------------------------------------------------------------------

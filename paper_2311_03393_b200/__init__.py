@@ -4,7 +4,7 @@ Argument marshalling only: every step of the path runs in libsketchmp.so's CUDA 
 PyTorch supplies device memory and the current CUDA stream.  The same names as the C-ABI:
 
     sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
-    sketch_plan, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
+    sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
     mp_selfjoin, discord_topk
 
 There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
@@ -62,6 +62,8 @@ _SIGS = {
     "skmp_last_error": (ctypes.c_char_p, []),
     "skmp_last_error_index": (_I64, []),
     "skmp_abi_version": (_I32, []),
+    "skmp_launch_count": (_I64, []),
+    "sketch_refresh": (ctypes.c_int, [_P, _P]),
     "sketch_hash_plan": (ctypes.c_int, [_P, _I64, _I32, ctypes.c_uint64, _P, _P]),
     "sketch_build": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, ctypes.POINTER(SketchCfg), _P, ctypes.POINTER(_P)]),
     "sketch_add_dim": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P]),
@@ -263,6 +265,14 @@ def sketch_plan(sk: Sketch):
     sg = np.empty(d)
     _check(lib().sketch_plan(sk.handle, _ptr(ids), _ptr(g), _ptr(s), _ptr(mu), _ptr(sg)))
     return dict(ids=ids, groups=g, signs=s, mu=mu, sigma=sg)
+
+
+def sketch_refresh(sk: Sketch, stream=None):
+    _check(lib().sketch_refresh(sk.handle, _stream(stream)))
+
+
+def skmp_launch_count() -> int:
+    return int(lib().skmp_launch_count())
 
 
 def sketch_free(sk: Sketch):

@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -20,9 +21,11 @@
 namespace {
 thread_local std::string g_msg;
 thread_local int64_t g_index = -1;
+std::atomic<int64_t> g_launches{0};
 }  // namespace
 
 namespace skmp {
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 skmp_status set_error(skmp_status s, const std::string& msg, int64_t index) {
   g_msg = msg;
   g_index = index;
@@ -50,6 +53,18 @@ skmp_status require_device() {
   if (e != cudaSuccess || n == 0) {
     cudaGetLastError();
     return set_error(SKMP_E_CUDA, "no CUDA device available (the path has no CPU fallback)");
+  }
+  // keep stream-ordered temporaries cached in the device pool between calls (no OS round trip)
+  static thread_local int configured = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && configured != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    configured = dev;
   }
   return SKMP_OK;
 }
@@ -252,6 +267,7 @@ const char* skmp_status_string(skmp_status s) {
 const char* skmp_last_error(void) { return g_msg.c_str(); }
 int64_t skmp_last_error_index(void) { return g_index; }
 int32_t skmp_abi_version(void) { return SKMP_ABI_VERSION; }
+int64_t skmp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 skmp_status sketch_hash_plan(const uint64_t* ids, int64_t d, int32_t k, uint64_t seed,
                              int32_t* groups, int8_t* signs) {
@@ -477,6 +493,15 @@ skmp_status sketch_plan(const skmp_sketch* h, uint64_t* ids, int32_t* g, int8_t*
   if (s) memcpy(s, h->s.data(), d * sizeof(int8_t));
   if (mu) memcpy(mu, h->mu.data(), d * sizeof(double));
   if (sigma) memcpy(sigma, h->sigma.data(), d * sizeof(double));
+  return ok();
+}
+
+skmp_status sketch_refresh(skmp_sketch* h, void* stream) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "sketch_refresh: NULL handle");
+  if (h->R == h->R64) return ok();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SKMP_CUDA(launch_cast_r(h->R64, h->R, (int64_t)h->k * h->n, h->dtype, st));
+  h->st = st;
   return ok();
 }
 

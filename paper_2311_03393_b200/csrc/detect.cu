@@ -128,6 +128,7 @@ cudaError_t launch_combine(const void* P, int64_t ldp, int k, int64_t n_sub, int
     combine_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(P), ldp, k, n_sub, d_inert, C, G);
   else
     combine_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(P), ldp, k, n_sub, d_inert, C, G);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -149,6 +150,7 @@ cudaError_t launch_topk(double* C, const int32_t* G, const int64_t* I, int64_t l
     topk_iter_kernel<<<(unsigned)blocks, kTopThreads, 0, st>>>(C, G, I, ldi, n_sub, radius, d_res,
                                                                d_count, part, ticket, q);
   }
+  count_launches(top);
   return cudaGetLastError();
 }
 

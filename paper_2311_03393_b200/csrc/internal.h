@@ -113,6 +113,12 @@ cudaError_t launch_topk(double* C, const int32_t* G, const int64_t* I, int64_t l
                         size_t ws_bytes, cudaStream_t st);
 size_t topk_ws_bytes(int64_t n_sub);
 
+// kernel-launch accounting (skmp_launch_count): every launcher reports its launches
+void count_launches(int64_t n);
+
+// R = dtype(R64) (sketch_refresh)
+cudaError_t launch_cast_r(const double* R64, void* R, int64_t count, int dtype, cudaStream_t st);
+
 // host hash (hash.cpp)
 void cw_params(uint64_t seed, uint64_t* a, uint64_t* b, uint64_t* c, uint64_t* e);
 void hash_plan(const uint64_t* ids, int64_t d, int32_t k, uint64_t seed, int32_t* g, int8_t* s);

@@ -109,6 +109,7 @@ cudaError_t launch_mp_finalize(const MpDev& w, void* P, int64_t* I, cudaStream_t
     finalize_kernel<float><<<grid, 256, 0, st>>>(w, w.nflat, static_cast<float*>(P), I);
   else
     finalize_kernel<double><<<grid, 256, 0, st>>>(w, w.nflat, static_cast<double*>(P), I);
+  count_launches(1);
   return cudaGetLastError();
 }
 

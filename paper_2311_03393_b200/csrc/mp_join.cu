@@ -457,6 +457,7 @@ cudaError_t launch_join_t(const MpDev& w, int64_t dlo, int64_t dhi, const int64_
   if (e) return e;
   dim3 grid((unsigned)ntiles, (unsigned)w.k);
   join_kernel<T, D, NT, C><<<grid, NT, smem, st>>>(a);
+  count_launches(1);
   return cudaGetLastError();
 }
 

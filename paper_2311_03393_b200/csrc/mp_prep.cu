@@ -174,6 +174,7 @@ cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st) {
     }
     prep_kernel<double><<<grid, kPrepThreads, smem, st>>>(w);
   }
+  count_launches(2);
   return cudaGetLastError();
 }
 
@@ -181,6 +182,7 @@ cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st) {
   const int words = w.dtype == SKMP_F32 ? 1 : 2;
   const int64_t count = (int64_t)w.k * w.n_sub;
   keys_init_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(w.keys, count, words);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -201,6 +203,7 @@ cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream
   e = cudaMemcpyAsync(d_ids, h_ids, sizeof(int32_t) * nser, cudaMemcpyHostToDevice, st);
   if (e) return e;
   flat_list_kernel<<<nser, 1024, 0, st>>>(w.flat, w.ldq, w.n_sub, w.flat_list, d_ids);
+  count_launches(1);
   e = cudaGetLastError();
   if (e) return e;
   e = cudaStreamSynchronize(st);  // h_ids must outlive the copy

@@ -356,7 +356,21 @@ __global__ void project_dense_kernel(const T* __restrict__ Tm, int64_t ld, int64
   }
 }
 
+__global__ void cast_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t count) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+
 }  // namespace
+
+cudaError_t launch_cast_r(const double* R64, void* R, int64_t count, int dtype, cudaStream_t st) {
+  if (dtype != SKMP_F32) return cudaSuccess;
+  const int64_t blocks = (count + 255) / 256;
+  cast_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, st>>>(R64, static_cast<float*>(R), count);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 size_t stats_ws_bytes(int64_t d, int64_t n) {
   const int64_t nchunks = (n + kStatsChunk - 1) / kStatsChunk;
@@ -389,6 +403,7 @@ cudaError_t launch_stream_stats(const void* T, int64_t d, int64_t n, int64_t ld,
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  count_launches((d + 65534) / 65535 + 1);
   stats_combine_kernel<<<(unsigned)((d + 127) / 128), 128, 0, st>>>(static_cast<Partial*>(ws), d,
                                                                    nchunks, out);
   return cudaGetLastError();
@@ -409,6 +424,7 @@ cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype
     project_count_kernel<double><<<grid, kProjThreads, 0, st>>>(
         static_cast<const double*>(T), ld, n, plan, mode, R64, static_cast<double*>(R), vec);
   }
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -425,6 +441,7 @@ cudaError_t launch_project_dense(const void* T, int64_t ld, int64_t n, int dtype
     project_dense_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(T), ld, n, k,
                                                        nstreams, S, ldS, mu, inv, mode, R64,
                                                        static_cast<double*>(R));
+  count_launches(1);
   return cudaGetLastError();
 }
 
