@@ -179,6 +179,10 @@ skmp_status mp_keys(skmp_mp* w, void** keys, int64_t* count, int32_t* words);
 skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, int32_t band,
                     int64_t* diag_lo, int64_t* diag_hi);
 
+/* Host-only: the join's tile width W (diagonals per tile) for dtype; band edges of mp_band are
+ * multiples of it. */
+int32_t mp_tile_width(int32_t dtype);
+
 /* Finalize: keys -> P [dev] k x n_sub (dtype) and I [dev] k x n_sub (int64), inert [host] k.
  * Requires the full diagonal range to have been joined.  Synchronous only for the inert copy.
  * Errors: INVALID_ARG, CUDA. */

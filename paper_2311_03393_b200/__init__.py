@@ -76,6 +76,7 @@ _SIGS = {
     "mp_create": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, ctypes.POINTER(_P)]),
     "mp_join": (ctypes.c_int, [_P, _I64, _I64, _P]),
     "mp_keys": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
+    "mp_tile_width": (_I32, [_I32]),
     "mp_band": (ctypes.c_int, [_I64, _I32, _I32, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "mp_finalize": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "mp_free": (None, [_P]),
@@ -160,6 +161,10 @@ def sketch_hash_plan(ids, k: int, seed: int):
     s = np.empty(len(ids), dtype=np.int8)
     _check(lib().sketch_hash_plan(_ptr(ids), len(ids), k, seed, _ptr(g), _ptr(s)))
     return g, s
+
+
+def mp_tile_width(dtype: int) -> int:
+    return int(lib().mp_tile_width(dtype))
 
 
 def mp_band(n_sub: int, excl: int, dtype: int, nbands: int, band: int):

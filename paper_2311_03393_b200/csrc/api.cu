@@ -657,6 +657,8 @@ skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, 
   return ok();
 }
 
+int32_t mp_tile_width(int32_t dtype) { return join_width(dtype == SKMP_F64 ? SKMP_F64 : SKMP_F32); }
+
 skmp_status mp_join(skmp_mp* h, int64_t diag_lo, int64_t diag_hi, void* stream) {
   if (!h) return set_error(SKMP_E_INVALID_ARG, "mp_join: NULL workspace");
   if (diag_lo < 0 || diag_hi < 0 || (diag_hi < diag_lo))

@@ -35,11 +35,12 @@ constexpr double kFlatEps = 1e-12;  // readings 4/5
 
 // Join geometry (see mp_join.cu).  The tile width W = NT*D diagonals is also the band
 // rounding unit of mp_band; rows per chunk C; a tile spans `reseed_rows` rows.
-constexpr int kJoinNT = 128;
-constexpr int kJoinD32 = 8;
+constexpr int kJoinNT = 32;   // one warp per CTA: no CTA-wide barriers in the hot loop
+constexpr int kJoinD32 = 8;    // default diagonals per thread (FP32); 16 selectable (SKMP_JOIN_D)
 constexpr int kJoinD64 = 8;
 constexpr int kJoinC = 32;
-inline int join_width(int dtype) { return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : kJoinD32); }
+int join_d32();                // diagonals per thread of the FP32 join (env SKMP_JOIN_D: 8 | 16)
+inline int join_width(int dtype) { return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : join_d32()); }
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
 inline int64_t join_pad(int dtype) { return join_width(dtype) + 4 * kJoinC + 64; }
 

@@ -29,6 +29,7 @@
 //    is independent of how diagonals are split into bands/GPUs -> bit-identical keys.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -59,6 +60,7 @@ struct JoinArgs {
   int m;
   int L;
   int64_t dlo, dhi;
+  unsigned eight;         // = 8 (runtime value on purpose, see join_tile)
   const int64_t* prefix;  // nblk + 1 cumulative tile counts
   int64_t nblk;
   int64_t blk0;
@@ -80,15 +82,34 @@ __device__ __forceinline__ double unord64(int64_t o) {
   return __longlong_as_double(o >= 0 ? o : (o ^ 0x7FFFFFFFFFFFFFFFll));
 }
 
-template <int D>
-__device__ __forceinline__ float code(float r, int d) {
-  return __int_as_float((__float_as_int(r) & ~(D - 1)) | d);
+// (bits & mask) | d as ONE LOP3 (LUT 0xEC = (a & c) | b): the slot code d is the immediate and
+// the mask ~(D-1) lives in one register shared by every slot, so ptxas neither splits the
+// operation into AND + OR nor materialises a register per code.
+template <int d>
+__device__ __forceinline__ unsigned lop_code_d(unsigned bits, unsigned mask) {
+  unsigned out;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(out) : "r"(bits), "n"(d), "r"(mask));
+  return out;
 }
-template <int D>
-__device__ __forceinline__ double code(double r, int d) {
+template <int d>
+__device__ __forceinline__ float code(float r, unsigned mask) {
+  return __uint_as_float(lop_code_d<d>(__float_as_uint(r), mask));
+}
+template <int d>
+__device__ __forceinline__ double code(double r, unsigned mask) {
   const int lo = __double2loint(r), hi = __double2hiint(r);
-  return __hiloint2double(hi, (lo & ~(D - 1)) | d);
+  return __hiloint2double(hi, (int)lop_code_d<d>((unsigned)lo, mask));
 }
+template <typename T, int d0, int n> struct Coder {
+  // k[d] = code<d>(rho[d]) for d in [d0, d0+n), d a compile-time immediate
+  __device__ static __forceinline__ void run(T* k, const T* rho, unsigned mask) {
+    k[d0] = code<d0>(rho[d0], mask);
+    Coder<T, d0 + 1, n - 1>::run(k, rho, mask);
+  }
+};
+template <typename T, int d0> struct Coder<T, d0, 0> {
+  __device__ static __forceinline__ void run(T*, const T*, unsigned) {}
+};
 template <int D>
 __device__ __forceinline__ int slot_of(float r) { return __float_as_int(r) & (D - 1); }
 template <int D>
@@ -102,6 +123,26 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 __device__ __forceinline__ double max3(double a, double b, double c) { return fmax(a, fmax(b, c)); }
 __device__ __forceinline__ float max2(float a, float b) { return fmaxf(a, b); }
 __device__ __forceinline__ double max2(double a, double b) { return fmax(a, b); }
+
+// max of n values with 3-input FMNMX3 where possible: ceil((n-1)/2) operations
+template <typename T, int N>
+__device__ __forceinline__ T tree_max(const T* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return max2(v[0], v[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    T w[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      if (3 * q + 2 < N) w[q] = max3(v[3 * q], v[3 * q + 1], v[3 * q + 2]);
+      else if (3 * q + 1 < N) w[q] = max2(v[3 * q], v[3 * q + 1]);
+      else w[q] = v[3 * q];
+    }
+    return tree_max<T, M>(w);
+  }
+}
 
 template <typename T> __device__ __forceinline__ T neg_inf();
 template <> __device__ __forceinline__ float neg_inf<float>() { return __int_as_float(0xff800000); }
@@ -153,6 +194,31 @@ __device__ __forceinline__ void publish(int64_t* keys, int64_t i, double v, int6
   }
 }
 
+// Rare path: a row / column candidate beat its shared-memory threshold.  Out of line so that
+// none of its address arithmetic is hoisted into the hot loop.
+template <typename T, int D>
+__device__ __noinline__ void publish_pair(int64_t* keys, T* rthr, T* cthr, int rb_u, int ct0, int ct1,
+                                          int64_t i_u, int64_t dt, T rowa, T rowb, T colv0, T colv1) {
+  if (rowa > rthr[rb_u]) {
+    publish(keys, i_u, rowa, i_u + dt + slot_of<D>(rowa));
+    rthr[rb_u] = rowa;
+  }
+  if (rowb > rthr[rb_u + 1]) {
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt + slot_of<D>(rowb));
+    rthr[rb_u + 1] = rowb;
+  }
+  if (colv0 > cthr[ct0]) {
+    const int64_t c = i_u + dt;
+    publish(keys, c, colv0, c - dt - slot_of<D>(colv0));
+    cthr[ct0] = colv0;
+  }
+  if (colv1 > cthr[ct1]) {
+    const int64_t c = i_u + 1 + dt;
+    publish(keys, c, colv1, c - dt - slot_of<D>(colv1));
+    cthr[ct1] = colv1;
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -168,6 +234,7 @@ struct Geo {
   static constexpr int RSD = RS / D;     // ring rows of the swizzled [D][RSD] layout
   static_assert(RS % D == 0, "ring must be a multiple of D");
   static_assert(C % (2 * D) == 0, "chunk must hold whole pairs of D-row rotations");
+  static_assert((C & (C - 1)) == 0, "C must be a power of two (row buffer index masking)");
   using Q = typename JT<T>::Q;
   static constexpr size_t smem_bytes =
       sizeof(Q) * (RS + 2 * C) + sizeof(T) * (RS + 2 * C);
@@ -184,6 +251,97 @@ __device__ __forceinline__ void stage_q(typename JT<T>::Q* dst, const typename J
 #pragma unroll
   for (int q = 0; q < parts; ++q)
     cp_async16(reinterpret_cast<char*>(dst) + 16 * q, reinterpret_cast<const char*>(src) + 16 * q);
+}
+
+// FP32 key of one cell (no ALU work): y = rho + 2 in [1, 4) computed by the FFMA that also
+// applies inv_i, then the slot code is appended below y's bits by ONE integer multiply-add
+// (FMA pipe): key = (bits(y) - bits(1.0)) * 8 + d, a positive float bit pattern whose order is
+// y's order.  The D slots of a row / column therefore reduce with plain FMNMX(3).
+template <int d>
+__device__ __forceinline__ float key32(float u, float inv_i, unsigned eight) {
+  const float y = fmaf(u, inv_i, 2.0f);
+  unsigned k;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(eight), "n"(0x04000000 + d));
+  return __uint_as_float(k);
+}
+template <typename T, int d0, int n> struct Keyer {
+  // k[d] = key of slot d for d in [d0, d0+n) (compile-time d)
+  __device__ static __forceinline__ void run(T* k, const T* u, T inv_i, unsigned aux) {
+    if constexpr (sizeof(T) == 4) {
+      k[d0] = key32<d0>(u[d0], inv_i, aux);
+    } else {
+      k[d0] = code<d0>(u[d0] * inv_i, aux);  // FP64: rho with the slot in its low mantissa bits
+    }
+    Keyer<T, d0 + 1, n - 1>::run(k, u, inv_i, aux);
+  }
+};
+template <typename T, int d0> struct Keyer<T, d0, 0> {
+  __device__ static __forceinline__ void run(T*, const T*, T, unsigned) {}
+};
+
+// One rotation: D consecutive rows ib .. ib+D-1 (processed as D/2 row pairs) of this thread's D
+// diagonals.  X[(u + d) % D] holds the operands of column ib + u + dt + d at row ib + u.
+template <typename T, int D, int RSD, bool MASKED>
+__device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D], T (&CK)[D],
+                                         const typename JT<T>::Q* rowp,
+                                         const typename JT<T>::Q* ring0,
+                                         const typename JT<T>::Q* ring1, const T* rthp,
+                                         const T* cth0, T* rthr, T* cthr, int rb, int qt,
+                                         int64_t ib, int64_t dt, const int (&lim)[D],
+                                         int64_t* keys, unsigned aux) {
+  using Q = typename JT<T>::Q;
+#pragma unroll
+  for (int u = 0; u < D; u += 2) {
+    // -- row u --
+    const Q ra = rowp[u];
+    X[(u + D - 1) % D] = (u == 0) ? ring0[((u + D - 1) % D) * RSD] : ring1[((u + D - 1) % D) * RSD];
+    T ka[D], uu[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const Q& x = X[(u + d) % D];
+      cov[d] = fma(ra.x, x.y, cov[d]);
+      cov[d] = fma(x.x, ra.y, cov[d]);
+      uu[d] = cov[d] * x.z;
+    }
+    Keyer<T, 0, D>::run(ka, uu, ra.z, aux);
+    if (MASKED) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) ka[d] = ((int)ib + u < lim[d]) ? ka[d] : neg_inf<T>();
+    }
+    // -- row u+1 (its entering column reuses the register of row u's completed column) --
+    const Q rbq = rowp[u + 1];
+    const T colv0 = max2(CK[u % D], ka[0]);  // column ib+u+dt completes after row u
+    X[u % D] = ring1[(u % D) * RSD];
+    T kb[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const Q& x = X[(u + 1 + d) % D];
+      cov[d] = fma(rbq.x, x.y, cov[d]);
+      cov[d] = fma(x.x, rbq.y, cov[d]);
+      uu[d] = cov[d] * x.z;
+    }
+    Keyer<T, 0, D>::run(kb, uu, rbq.z, aux);
+    if (MASKED) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) kb[d] = ((int)ib + u + 1 < lim[d]) ? kb[d] : neg_inf<T>();
+    }
+    // -- column maxima: registers x = (u + d) % D --
+    const T colv1 = max3(CK[(u + 1) % D], ka[1], kb[0]);  // column ib+u+1+dt completes
+#pragma unroll
+    for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = max3(CK[(u + d) % D], ka[d], kb[d - 1]);
+    CK[(u + D - 1) % D] = max2(ka[D - 1], kb[D - 2]);  // column entered at row u
+    CK[u % D] = kb[D - 1];                              // column entered at row u+1
+    // -- row maxima over the D slots --
+    const T rowa = tree_max<T, D>(ka);
+    const T rowb = tree_max<T, D>(kb);
+    // -- check-then-publish (rare) --
+    const bool hit = (rowa > rthp[u]) | (rowb > rthp[u + 1]) | (colv0 > cth0[(u % D) * RSD]) |
+                     (colv1 > cth0[((u + 1) % D) * RSD]);
+    if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
+      publish_pair<T, D>(keys, rthr, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+                         ib + u, dt, rowa, rowb, colv0, colv1);
+    }
+  }
 }
 
 template <typename T, int D, int NT, int C, bool MASKED>
@@ -206,12 +364,14 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   const int64_t dt = delta0 + (int64_t)tid * D;  // this thread's first diagonal
 
   // per-slot validity limit: cell (i, i+dt+d) is valid iff i < lim[d]
-  int64_t lim[D];
+  int lim[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const int64_t dd = dt + d;
-    lim[d] = (dd >= a.dlo && dd < a.dhi && dd < n_sub) ? (n_sub - dd) : 0;
+    lim[d] = (dd >= a.dlo && dd < a.dhi && dd < n_sub) ? (int)(n_sub - dd) : 0;
   }
+  // diagonals cut by the band edges: every chunk of this tile needs the per-cell mask
+  const bool diag_masked = (delta0 < a.dlo) || (delta0 + W > a.dhi);
 
   // ---- exact FP64 seed of cov(i0, i0+dt+d), pre-compensated for the first in-loop update -----
   T cov[D];
@@ -262,7 +422,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     rthr[i % (2 * C)] = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
   }
   cp_async_wait_all();
-  __syncthreads();
+  __syncthreads();  // (one warp per CTA: a warp barrier; kept generic for NT > 32)
 
   // column operand registers: X[(u + d) % D] holds column i + dt + d at unrolled row u
   Q X[D];
@@ -272,6 +432,11 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #pragma unroll
   for (int d = 0; d < D; ++d) CK[d] = neg_inf<T>();
 
+  // one register operand shared by all slot codes (opaque so ptxas keeps it a register):
+  // FP32: the multiplier 8 of the key IMAD; FP64: the LOP3 mask ~(D-1)
+  // (loaded from the kernel parameters so ptxas cannot strength-reduce the IMAD into an ALU LEA)
+  const unsigned aux = (sizeof(T) == 4) ? a.eight : (unsigned)~(D - 1);
+
   // ring row index of column (ib + dt): qt; (ib + dt) is a multiple of D
   int qt = (int)(((i0 + dt) % RS) / D);
 
@@ -279,104 +444,49 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     const int64_t rend = (r + C < i1) ? r + C : i1;
     // ---- prefetch the next chunk: rows [r+C, r+2C), columns [r+delta0+W+C, +C) --------------
     const bool more = r + C < i1;
-    T nthr_c = pos_inf<T>(), nthr_r = pos_inf<T>();
-    int64_t nc = -1, nr = -1;
+    // each thread stages CPT columns and CPT rows of the next chunk (C = CPT * NT)
+    constexpr int CPT = C / NT;
+    static_assert(C % NT == 0, "chunk rows must be a multiple of the CTA size");
+    T nthr_c[CPT], nthr_r[CPT];
     if (more) {
-      if (tid < C) {
-        nc = r + delta0 + W + C + tid;
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) {
+        const int64_t nc = r + delta0 + W + C + tid + e * NT;
         stage_q<T>(&ring[G::pos(nc)], &q[nc]);
-        if (nc < n_sub) nthr_c = load_thr(keys, nc, (T*)nullptr);
-      } else if (tid < 2 * C) {
-        nr = r + C + (tid - C);
+        nthr_c[e] = (nc < n_sub) ? load_thr(keys, nc, (T*)nullptr) : pos_inf<T>();
+        const int64_t nr = r + C + tid + e * NT;
         stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
-        if (nr < n_sub) nthr_r = load_thr(keys, nr, (T*)nullptr);
+        nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) : pos_inf<T>();
       }
     }
 
     // ---- compute rows [r, rend) in D-row rotations of 2-row pairs ---------------------------
-    for (int64_t ib = r; ib < rend; ib += D) {
+    // 32-bit bookkeeping only: rb = ib mod 2C (row buffer), qt = ring row of column ib + dt.
+    const int nrot = (int)((rend - r) / D);
+    int rb = (int)(r & (2 * C - 1));
+    int64_t ib = r;
+    // the chunk needs per-cell masks only where it reaches the triangle edge (i + delta >= n_sub)
+    // or the band's diagonal edges
+    const bool cmasked = MASKED && (diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub);
+    for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
-      const int rb = (int)(ib % (2 * C));
-#pragma unroll
-      for (int u = 0; u < D; u += 2) {
-        // -- row u --
-        const Q ra = rowq[rb + u];
-        X[(u + D - 1) % D] = ring[((u + D - 1) % D) * RSD + (u == 0 ? qt : qt1)];
-        T ka[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const Q& x = X[(u + d) % D];
-          cov[d] = fma(ra.x, x.y, cov[d]);
-          cov[d] = fma(x.x, ra.y, cov[d]);
-          const T rho = (cov[d] * x.z) * ra.z;
-          ka[d] = code<D>(rho, d);
-          if (MASKED) ka[d] = (ib + u < lim[d]) ? ka[d] : neg_inf<T>();
-        }
-        // -- row u+1 (its entering column reuses the register of row u's completed column) --
-        const Q rbq = rowq[rb + u + 1];
-        const T colv0 = max2(CK[u % D], ka[0]);  // column ib+u+dt completes after row u
-        X[u % D] = ring[(u % D) * RSD + qt1];
-        T kb[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const Q& x = X[(u + 1 + d) % D];
-          cov[d] = fma(rbq.x, x.y, cov[d]);
-          cov[d] = fma(x.x, rbq.y, cov[d]);
-          const T rho = (cov[d] * x.z) * rbq.z;
-          kb[d] = code<D>(rho, d);
-          if (MASKED) kb[d] = (ib + u + 1 < lim[d]) ? kb[d] : neg_inf<T>();
-        }
-        // -- column maxima: registers x = (u + d) % D --
-        const T colv1 = max3(CK[(u + 1) % D], ka[1], kb[0]);  // column ib+u+1+dt completes
-#pragma unroll
-        for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = max3(CK[(u + d) % D], ka[d], kb[d - 1]);
-        CK[(u + D - 1) % D] = max2(ka[D - 1], kb[D - 2]);  // column entered at row u
-        CK[u % D] = kb[D - 1];                              // column entered at row u+1
-        // -- row maxima over the D slots --
-        T rowa, rowb;
-        if (D == 8) {
-          rowa = max3(max3(ka[0], ka[1], ka[2]), max3(ka[3], ka[4], ka[5]), max2(ka[6], ka[7]));
-          rowb = max3(max3(kb[0], kb[1], kb[2]), max3(kb[3], kb[4], kb[5]), max2(kb[6], kb[7]));
-        } else {
-          rowa = ka[0];
-          rowb = kb[0];
-#pragma unroll
-          for (int d = 1; d < D; ++d) { rowa = max2(rowa, ka[d]); rowb = max2(rowb, kb[d]); }
-        }
-        // -- check-then-publish --
-        const T ta = rthr[rb + u], tb = rthr[rb + u + 1];
-        const T tc0 = cthr[(u % D) * RSD + qt];
-        const T tc1 = cthr[((u + 1) % D) * RSD + qt];
-        if (rowa > ta || rowb > tb || colv0 > tc0 || colv1 > tc1) {
-          if (rowa > ta) {
-            const int64_t i = ib + u;
-            publish(keys, i, rowa, i + dt + slot_of<D>(rowa));
-            rthr[rb + u] = rowa;
-          }
-          if (rowb > tb) {
-            const int64_t i = ib + u + 1;
-            publish(keys, i, rowb, i + dt + slot_of<D>(rowb));
-            rthr[rb + u + 1] = rowb;
-          }
-          if (colv0 > tc0) {
-            const int64_t c = ib + u + dt;
-            publish(keys, c, colv0, c - dt - slot_of<D>(colv0));
-            cthr[(u % D) * RSD + qt] = colv0;
-          }
-          if (colv1 > tc1) {
-            const int64_t c = ib + u + 1 + dt;
-            publish(keys, c, colv1, c - dt - slot_of<D>(colv1));
-            cthr[((u + 1) % D) * RSD + qt] = colv1;
-          }
-        }
-      }
+      if (cmasked)
+        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, rthr + rb, cthr + qt,
+                                  rthr, cthr, rb, qt, ib, dt, lim, keys, aux);
+      else
+        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, rthr + rb, cthr + qt,
+                                   rthr, cthr, rb, qt, ib, dt, lim, keys, aux);
       qt = qt1;
+      rb = (rb + D) & (2 * C - 1);
     }
 
     // ---- land the prefetched chunk ------------------------------------------------------------
     if (more) {
-      if (nc >= 0) cthr[G::pos(nc)] = nthr_c;
-      if (nr >= 0) rthr[nr % (2 * C)] = nthr_r;
+#pragma unroll
+      for (int e = 0; e < CPT; ++e) {
+        cthr[G::pos(r + delta0 + W + C + tid + e * NT)] = nthr_c[e];
+        rthr[(r + C + tid + e * NT) % (2 * C)] = nthr_r[e];
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -424,10 +534,8 @@ join_kernel(JoinArgs a) {
   // rows are processed in whole D-row rotations; rows beyond i1 are masked cells
   const int64_t i1r = i0 + (((i1 - i0) + D - 1) / D) * D;
   const bool masked = (delta0 < a.dlo) || (delta0 + W > a.dhi) || (i1r - 1 + delta0 + W - 1 >= a.n_sub);
-  if (masked)
-    join_tile<T, D, NT, C, true>(a, g, delta0, i0, i1r, smem_raw);
-  else
-    join_tile<T, D, NT, C, false>(a, g, delta0, i0, i1r, smem_raw);
+  (void)masked;  // masking is decided per chunk inside the tile
+  join_tile<T, D, NT, C, true>(a, g, delta0, i0, i1r, smem_raw);
 }
 
 template <typename T, int D>
@@ -449,6 +557,7 @@ cudaError_t launch_join_t(const MpDev& w, int64_t dlo, int64_t dhi, const int64_
   a.dlo = dlo;
   a.dhi = dhi;
   a.prefix = prefix;
+  a.eight = 8;
   a.nblk = nblk;
   a.blk0 = blk0;
   const size_t smem = G::smem_bytes;
@@ -463,10 +572,22 @@ cudaError_t launch_join_t(const MpDev& w, int64_t dlo, int64_t dhi, const int64_
 
 }  // namespace
 
+int join_d32() {
+  static const int d = [] {
+    const char* e = getenv("SKMP_JOIN_D");
+    const int v = e ? atoi(e) : kJoinD32;
+    return (v == 16) ? 16 : 8;
+  }();
+  return d;
+}
+
 cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_prefix,
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
-  if (w.dtype == SKMP_F32) return launch_join_t<float, kJoinD32>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+  if (w.dtype == SKMP_F32) {
+    if (join_d32() == 16) return launch_join_t<float, 16>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+    return launch_join_t<float, 8>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+  }
   return launch_join_t<double, kJoinD64>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
 }
 

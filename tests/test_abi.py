@@ -57,7 +57,7 @@ def test_hash_plan_invalid():
 
 @pytest.mark.parametrize("n_sub,excl,dtype", [(1999745, 128, 0), (199745, 128, 0), (19901, 50, 1), (1951, 25, 1)])
 def test_band_partition(n_sub, excl, dtype):
-    W = 128 * 8
+    W = skmp.mp_tile_width(dtype)
     for nb in (1, 2, 4, 8):
         edges = []
         for b in range(nb):
