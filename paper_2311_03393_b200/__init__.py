@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsketchmp.so")
+LIB_PATH = os.environ.get("SKMP_LIB") or os.path.join(_HERE, "libsketchmp.so")
 
 F32, F64 = 0, 1
 PROJ_COUNT_SKETCH, PROJ_DENSE = 0, 1

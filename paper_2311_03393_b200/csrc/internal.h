@@ -6,7 +6,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/sketchmp.h"
+#include "sketchmp.h"
 
 namespace skmp {
 
@@ -38,7 +38,10 @@ constexpr double kFlatEps = 1e-12;  // readings 4/5
 constexpr int kJoinNT = 32;   // one warp per CTA: no CTA-wide barriers in the hot loop
 constexpr int kJoinD32 = 8;    // default diagonals per thread (FP32); 16 selectable (SKMP_JOIN_D)
 constexpr int kJoinD64 = 8;
-constexpr int kJoinC = 32;
+#ifndef SKMP_JOIN_C
+#define SKMP_JOIN_C 32
+#endif
+constexpr int kJoinC = SKMP_JOIN_C;  // rows per staged chunk (power of two, multiple of 2D)
 int join_d32();                // diagonals per thread of the FP32 join (env SKMP_JOIN_D: 8 | 16)
 inline int join_width(int dtype) { return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : join_d32()); }
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
@@ -99,6 +102,10 @@ cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
 // band join: tiles described by blocks of W diagonals [dlo, dhi)
 cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
+// packed f32x2 FP32 join (mp_join_x2.cu), opt-in with SKMP_JOIN_IMPL=x2
+bool join_x2_enabled();
+cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
+                              int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
 cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);
 cudaError_t launch_mp_finalize(const MpDev& w, void* P, int64_t* I, cudaStream_t st);
 

@@ -32,167 +32,12 @@
 #include <stdlib.h>
 
 #include "internal.h"
+#include "join_common.cuh"
 
 namespace skmp {
 namespace {
+using namespace join;
 
-struct __align__(32) dq4 { double x, y, z, w; };
-
-template <typename T> struct JT;
-template <> struct JT<float> {
-  using Q = float4;
-  static constexpr int D = kJoinD32;
-};
-template <> struct JT<double> {
-  using Q = dq4;
-  static constexpr int D = kJoinD64;
-};
-
-struct JoinArgs {
-  const void* R;
-  int64_t ld;
-  const void* Q;
-  const double* mu;
-  int64_t ldq;
-  int64_t* keys;
-  int64_t n_sub;
-  int64_t n;
-  int m;
-  int L;
-  int64_t dlo, dhi;
-  unsigned eight;         // = 8 (runtime value on purpose, see join_tile)
-  const int64_t* prefix;  // nblk + 1 cumulative tile counts
-  int64_t nblk;
-  int64_t blk0;
-};
-
-// ---- key encodings ------------------------------------------------------------------------
-__device__ __forceinline__ int32_t ord32(float f) {
-  const int32_t b = __float_as_int(f);
-  return b >= 0 ? b : (b ^ 0x7FFFFFFF);
-}
-__device__ __forceinline__ float unord32(int32_t o) {
-  return __int_as_float(o >= 0 ? o : (o ^ 0x7FFFFFFF));
-}
-__device__ __forceinline__ int64_t ord64(double f) {
-  const int64_t b = __double_as_longlong(f);
-  return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFll);
-}
-__device__ __forceinline__ double unord64(int64_t o) {
-  return __longlong_as_double(o >= 0 ? o : (o ^ 0x7FFFFFFFFFFFFFFFll));
-}
-
-// (bits & mask) | d as ONE LOP3 (LUT 0xEC = (a & c) | b): the slot code d is the immediate and
-// the mask ~(D-1) lives in one register shared by every slot, so ptxas neither splits the
-// operation into AND + OR nor materialises a register per code.
-template <int d>
-__device__ __forceinline__ unsigned lop_code_d(unsigned bits, unsigned mask) {
-  unsigned out;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(out) : "r"(bits), "n"(d), "r"(mask));
-  return out;
-}
-template <int d>
-__device__ __forceinline__ float code(float r, unsigned mask) {
-  return __uint_as_float(lop_code_d<d>(__float_as_uint(r), mask));
-}
-template <int d>
-__device__ __forceinline__ double code(double r, unsigned mask) {
-  const int lo = __double2loint(r), hi = __double2hiint(r);
-  return __hiloint2double(hi, (int)lop_code_d<d>((unsigned)lo, mask));
-}
-template <typename T, int d0, int n> struct Coder {
-  // k[d] = code<d>(rho[d]) for d in [d0, d0+n), d a compile-time immediate
-  __device__ static __forceinline__ void run(T* k, const T* rho, unsigned mask) {
-    k[d0] = code<d0>(rho[d0], mask);
-    Coder<T, d0 + 1, n - 1>::run(k, rho, mask);
-  }
-};
-template <typename T, int d0> struct Coder<T, d0, 0> {
-  __device__ static __forceinline__ void run(T*, const T*, unsigned) {}
-};
-template <int D>
-__device__ __forceinline__ int slot_of(float r) { return __float_as_int(r) & (D - 1); }
-template <int D>
-__device__ __forceinline__ int slot_of(double r) { return __double2loint(r) & (D - 1); }
-
-__device__ __forceinline__ float max3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-__device__ __forceinline__ double max3(double a, double b, double c) { return fmax(a, fmax(b, c)); }
-__device__ __forceinline__ float max2(float a, float b) { return fmaxf(a, b); }
-__device__ __forceinline__ double max2(double a, double b) { return fmax(a, b); }
-
-// max of n values with 3-input FMNMX3 where possible: ceil((n-1)/2) operations
-template <typename T, int N>
-__device__ __forceinline__ T tree_max(const T* v) {
-  if constexpr (N == 1) {
-    return v[0];
-  } else if constexpr (N == 2) {
-    return max2(v[0], v[1]);
-  } else {
-    constexpr int M = (N + 2) / 3;
-    T w[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
-      if (3 * q + 2 < N) w[q] = max3(v[3 * q], v[3 * q + 1], v[3 * q + 2]);
-      else if (3 * q + 1 < N) w[q] = max2(v[3 * q], v[3 * q + 1]);
-      else w[q] = v[3 * q];
-    }
-    return tree_max<T, M>(w);
-  }
-}
-
-template <typename T> __device__ __forceinline__ T neg_inf();
-template <> __device__ __forceinline__ float neg_inf<float>() { return __int_as_float(0xff800000); }
-template <> __device__ __forceinline__ double neg_inf<double>() {
-  return __longlong_as_double(0xfff0000000000000ll);
-}
-template <typename T> __device__ __forceinline__ T pos_inf();
-template <> __device__ __forceinline__ float pos_inf<float>() { return __int_as_float(0x7f800000); }
-template <> __device__ __forceinline__ double pos_inf<double>() {
-  return __longlong_as_double(0x7ff0000000000000ll);
-}
-
-// threshold (current global best rho) of profile entry i
-__device__ __forceinline__ float load_thr(const int64_t* keys, int64_t i, float*) {
-  const int64_t k = __ldcg(keys + i);
-  return unord32((int32_t)(k >> 32));
-}
-__device__ __forceinline__ double load_thr(const int64_t* keys, int64_t i, double*) {
-  const int64_t k = __ldcg(keys + 2 * i);
-  return unord64(k);
-}
-
-// publish candidate (v, arg) into profile entry i
-__device__ __forceinline__ void publish(int64_t* keys, int64_t i, float v, int64_t arg) {
-  const int64_t key = (int64_t)(((uint64_t)(uint32_t)ord32(v) << 32) |
-                                (uint64_t)(0xFFFFFFFFu - (uint32_t)arg));
-  atomicMax(reinterpret_cast<long long*>(keys + i), (long long)key);
-}
-__device__ __forceinline__ void publish(int64_t* keys, int64_t i, double v, int64_t arg) {
-  // entry = {w0: orderable(rho), w1: -1 - j} at p[0], p[1]; lexicographic max via 128-bit CAS
-  // (the b128 register {lo, hi} maps lo to the lower address).
-  const int64_t n0 = ord64(v), n1 = -1 - arg;
-  int64_t* p = keys + 2 * i;
-  int64_t o0 = __ldcg(p), o1 = __ldcg(p + 1);
-  while (n0 > o0 || (n0 == o0 && n1 > o1)) {
-    int64_t r0, r1;
-    asm volatile(
-        "{ .reg .b128 c, s, o;\n"
-        "  mov.b128 c, {%2, %3};\n"
-        "  mov.b128 s, {%4, %5};\n"
-        "  atom.global.cas.b128 o, [%6], c, s;\n"
-        "  mov.b128 {%0, %1}, o; }"
-        : "=l"(r0), "=l"(r1)
-        : "l"(o0), "l"(o1), "l"(n0), "l"(n1), "l"(p)
-        : "memory");
-    if (r0 == o0 && r1 == o1) break;
-    o0 = r0;
-    o1 = r1;
-  }
-}
 
 // Rare path: a row / column candidate beat its shared-memory threshold.  Out of line so that
 // none of its address arithmetic is hoisted into the hot loop.
@@ -217,14 +62,6 @@ __device__ __noinline__ void publish_pair(int64_t* keys, T* rthr, T* cthr, int r
     publish(keys, c, colv1, c - dt - slot_of<D>(colv1));
     cthr[ct1] = colv1;
   }
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 template <typename T, int D, int NT, int C>
@@ -503,8 +340,11 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   }
 }
 
+#ifndef SKMP_JOIN_MINB
+#define SKMP_JOIN_MINB 20  // FP32 D=8: cap at ~96 registers -> 20 warps/SM (measured best)
+#endif
 template <typename T, int D, int NT, int C>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : 1))
 join_kernel(JoinArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = NT * D;
@@ -585,6 +425,8 @@ cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
   if (w.dtype == SKMP_F32) {
+    if (join_x2_enabled() && join_d32() == 8)
+      return launch_mp_join_x2(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
     if (join_d32() == 16) return launch_join_t<float, 16>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
     return launch_join_t<float, 8>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
   }

@@ -1,3 +1,3 @@
 python tools/join_bench.py
-python tools/join_bench.py --dtype f64 --k 16 --n 20000 --m 100
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+SKMP_JOIN_IMPL=x2 python tools/join_bench.py | sed 's/^/x2 /'
+SKMP_JOIN_IMPL=x2 timeout 600 python -m pytest tests/test_gpu_mp.py -q -x 2>&1 | tail -2
