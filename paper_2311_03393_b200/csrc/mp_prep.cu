@@ -28,8 +28,12 @@ __global__ void amax_kernel(const T* __restrict__ R, int64_t ld, int64_t n, doub
     a = fmax(a, fabs((double)r[t]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-  if ((threadIdx.x & 31) == 0) {
-    // non-negative doubles order like their bit patterns
+  __shared__ double wmax[8];
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a = fmax(a, wmax[w]);
+    // one atomic per block; non-negative doubles order like their bit patterns
     atomicMax(reinterpret_cast<unsigned long long*>(amax + g),
               (unsigned long long)__double_as_longlong(a));
   }
@@ -150,7 +154,7 @@ cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st) {
   e = cudaMemsetAsync(w.Q, 0, qsz * (size_t)w.k * (size_t)w.ldq, st);
   if (e) return e;
   {
-    const int64_t blocks = (w.n + 255) / 256;
+    const int64_t blocks = (w.n + 4095) / 4096;  // ~16 samples per thread
     dim3 grid((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)w.k);
     if (w.dtype == SKMP_F32)
       amax_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w.R), w.ld, w.n, w.amax);

@@ -20,58 +20,23 @@ namespace skmp {
 namespace {
 
 constexpr int kStatsThreads = 256;
-constexpr int kStatsPerThread = 16;
-constexpr int kStatsChunk = kStatsThreads * kStatsPerThread;  // 4096 samples per block
+constexpr int kStatsChunk = 32768;  // samples per block (128 KB of FP32)
 
 struct Partial {
   double cnt, mean, m2, amax;
 };
 
 template <typename T>
-__device__ __forceinline__ void load_chunk(const T* __restrict__ x, int64_t base, int64_t n,
-                                           double (&v)[kStatsPerThread], int& cnt, bool vec);
-
+__device__ __forceinline__ void vload4(const T* p, double* out);
 template <>
-__device__ __forceinline__ void load_chunk<float>(const float* __restrict__ x, int64_t base,
-                                                  int64_t n, double (&v)[kStatsPerThread],
-                                                  int& cnt, bool vec) {
-  // layout: element (it*256 + tid)*4 + q of the chunk, it = 0..3, q = 0..3 (coalesced float4)
-  cnt = 0;
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    int64_t e = base + ((int64_t)it * kStatsThreads + threadIdx.x) * 4;
-    if (vec && e + 4 <= n) {
-      float4 f = __ldcs(reinterpret_cast<const float4*>(x + e));
-      v[it * 4 + 0] = f.x; v[it * 4 + 1] = f.y; v[it * 4 + 2] = f.z; v[it * 4 + 3] = f.w;
-      cnt += 4;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (e + q < n) { v[it * 4 + q] = x[e + q]; ++cnt; } else { v[it * 4 + q] = 0.0; }
-      }
-    }
-  }
+__device__ __forceinline__ void vload4<float>(const float* p, double* out) {
+  const float4 f = __ldcs(reinterpret_cast<const float4*>(p));
+  out[0] = f.x; out[1] = f.y; out[2] = f.z; out[3] = f.w;
 }
-
 template <>
-__device__ __forceinline__ void load_chunk<double>(const double* __restrict__ x, int64_t base,
-                                                   int64_t n, double (&v)[kStatsPerThread],
-                                                   int& cnt, bool vec) {
-  cnt = 0;
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    int64_t e = base + ((int64_t)it * kStatsThreads + threadIdx.x) * 2;
-    if (vec && e + 2 <= n) {
-      double2 f = __ldcs(reinterpret_cast<const double2*>(x + e));
-      v[it * 2 + 0] = f.x; v[it * 2 + 1] = f.y;
-      cnt += 2;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (e + q < n) { v[it * 2 + q] = x[e + q]; ++cnt; } else { v[it * 2 + q] = 0.0; }
-      }
-    }
-  }
+__device__ __forceinline__ void vload4<double>(const double* p, double* out) {
+  const double2 f = __ldcs(reinterpret_cast<const double2*>(p));
+  out[0] = f.x; out[1] = f.y;
 }
 
 __device__ __forceinline__ double block_sum(double x, double* sh) {
@@ -100,48 +65,67 @@ __device__ __forceinline__ double block_max(double x, double* sh) {
   return t;
 }
 
-// K1a: per (stream, chunk) count, mean, M2 (two passes over registers), max|x|, finiteness.
+// K1a: per (stream, chunk) count, mean, M2, max|x|, finiteness.  A block streams a long chunk
+// (kStatsChunk samples) with U independent 16-byte loads in flight per thread and accumulates
+// shifted FP64 sums (x - K), (x - K)^2 with K = the chunk's first sample (the shift keeps the
+// one-pass M2 = S2 - S1^2/n well conditioned); one block reduction per chunk.
 template <typename T>
 __global__ void __launch_bounds__(kStatsThreads)
 stats_partial_kernel(const T* __restrict__ Tm, int64_t n, int64_t ld, int64_t nchunks,
                      Partial* __restrict__ part, int32_t* __restrict__ flag, bool vec) {
   __shared__ double sh[kStatsThreads / 32];
+  constexpr int VN = (sizeof(T) == 4) ? 4 : 2;
+  constexpr int U = (sizeof(T) == 4) ? 4 : 8;  // 16-byte loads in flight per thread
   const int64_t j = blockIdx.y;
   const int64_t c = blockIdx.x;
   const T* x = Tm + j * ld;
   const int64_t base = c * kStatsChunk;
-  double v[kStatsPerThread];
-  int cnt;
-  load_chunk<T>(x, base, n, v, cnt, vec);
-  const int64_t total = min((int64_t)kStatsChunk, n - base);
-  double s = 0.0, a = 0.0;
+  const int64_t end = (base + kStatsChunk < n) ? base + kStatsChunk : n;
+  const double K = (double)x[base];
+  double s1 = 0.0, s2 = 0.0, a = 0.0;
   bool finite = true;
+  const int64_t step = (int64_t)kStatsThreads * VN;
+  int64_t e = base + (int64_t)threadIdx.x * VN;
+  if (vec) {
+    for (; e + (U - 1) * step + VN <= end; e += U * step) {
+      double v[U][VN];
 #pragma unroll
-  for (int q = 0; q < kStatsPerThread; ++q) {
-    s += v[q];
-    a = fmax(a, fabs(v[q]));
-    finite &= isfinite(v[q]);
+      for (int u = 0; u < U; ++u) vload4<T>(x + e + u * step, v[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VN; ++q) {
+          const double dv = v[u][q] - K;
+          s1 += dv;
+          s2 = fma(dv, dv, s2);
+          a = fmax(a, fabs(v[u][q]));
+          finite &= isfinite(v[u][q]);
+        }
+    }
   }
-  // non-finite inputs poison the sums; flag them (the host reports NONFINITE)
+  for (; e < end; e += step) {  // tail (and the unaligned path) sample by sample
+#pragma unroll
+    for (int q = 0; q < VN; ++q) {
+      if (e + q < end) {
+        const double xv = (double)x[e + q];
+        const double dv = xv - K;
+        s1 += dv;
+        s2 = fma(dv, dv, s2);
+        a = fmax(a, fabs(xv));
+        finite &= isfinite(xv);
+      }
+    }
+  }
   if (!finite) atomicMax(flag + j, 1);
-  s = block_sum(s, sh);
-  const double mean = s / (double)total;
-  constexpr int VN = (sizeof(T) == 4) ? 4 : 2;
-  double q2 = 0.0;
-#pragma unroll
-  for (int q = 0; q < kStatsPerThread; ++q) {
-    const int64_t e = base + ((int64_t)(q / VN) * kStatsThreads + threadIdx.x) * VN + (q % VN);
-    const double dlt = (e < n) ? v[q] - mean : 0.0;  // padding slots contribute nothing
-    q2 += dlt * dlt;
-  }
-  (void)cnt;
-  q2 = block_sum(q2, sh);
+  s1 = block_sum(s1, sh);
+  s2 = block_sum(s2, sh);
   a = block_max(a, sh);
   if (threadIdx.x == 0) {
+    const double cnt = (double)(end - base);
     Partial p;
-    p.cnt = (double)total;
-    p.mean = mean;
-    p.m2 = fmax(q2, 0.0);
+    p.cnt = cnt;
+    p.mean = K + s1 / cnt;
+    p.m2 = fmax(s2 - s1 * (s1 / cnt), 0.0);
     p.amax = a;
     part[j * nchunks + c] = p;
   }
@@ -181,35 +165,6 @@ __global__ void stats_combine_kernel(const Partial* __restrict__ part, int64_t d
 constexpr int kProjThreads = 256;
 constexpr int kProjBatch = 256;
 
-template <typename T> struct VecOf;
-template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
-template <> struct VecOf<double> { using V = double2; static constexpr int N = 2; };
-
-template <typename T>
-__device__ __forceinline__ void vload(const T* p, double* out, int64_t e, int64_t n, bool vec);
-template <>
-__device__ __forceinline__ void vload<float>(const float* p, double* out, int64_t e, int64_t n,
-                                             bool vec) {
-  if (vec && e + 4 <= n) {
-    float4 f = __ldcs(reinterpret_cast<const float4*>(p + e));
-    out[0] = f.x; out[1] = f.y; out[2] = f.z; out[3] = f.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) out[q] = (e + q < n) ? (double)p[e + q] : 0.0;
-  }
-}
-template <>
-__device__ __forceinline__ void vload<double>(const double* p, double* out, int64_t e, int64_t n,
-                                              bool vec) {
-  if (vec && e + 2 <= n) {
-    double2 f = __ldcs(reinterpret_cast<const double2*>(p + e));
-    out[0] = f.x; out[1] = f.y;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 2; ++q) out[q] = (e + q < n) ? p[e + q] : 0.0;
-  }
-}
-
 template <typename T>
 __device__ __forceinline__ void store_out(T* R, int64_t e, int64_t n, const double* v);
 template <>
@@ -229,13 +184,47 @@ __device__ __forceinline__ void store_out<double>(double* R, int64_t e, int64_t 
   }
 }
 
+// raw 4-sample vector loads kept in the input precision until use
+template <typename T> struct Raw4;
+template <> struct Raw4<float> { float4 v; };
+template <> struct Raw4<double> { double2 a, b; };
+__device__ __forceinline__ void rload(Raw4<float>& r, const float* p, int64_t e, int64_t n, bool vec) {
+  if (vec && e + 4 <= n) {
+    r.v = __ldcs(reinterpret_cast<const float4*>(p + e));
+  } else {
+    r.v.x = (e + 0 < n) ? p[e + 0] : 0.f;
+    r.v.y = (e + 1 < n) ? p[e + 1] : 0.f;
+    r.v.z = (e + 2 < n) ? p[e + 2] : 0.f;
+    r.v.w = (e + 3 < n) ? p[e + 3] : 0.f;
+  }
+}
+__device__ __forceinline__ void rload(Raw4<double>& r, const double* p, int64_t e, int64_t n, bool vec) {
+  if (vec && e + 4 <= n) {
+    r.a = __ldcs(reinterpret_cast<const double2*>(p + e));
+    r.b = __ldcs(reinterpret_cast<const double2*>(p + e + 2));
+  } else {
+    r.a.x = (e + 0 < n) ? p[e + 0] : 0.0;
+    r.a.y = (e + 1 < n) ? p[e + 1] : 0.0;
+    r.b.x = (e + 2 < n) ? p[e + 2] : 0.0;
+    r.b.y = (e + 3 < n) ? p[e + 3] : 0.0;
+  }
+}
+__device__ __forceinline__ double rget(const Raw4<float>& r, int q) {
+  return q == 0 ? r.v.x : q == 1 ? r.v.y : q == 2 ? r.v.z : r.v.w;
+}
+__device__ __forceinline__ double rget(const Raw4<double>& r, int q) {
+  return q == 0 ? r.a.x : q == 1 ? r.a.y : q == 2 ? r.b.x : r.b.y;
+}
+
+// K2: count-sketch projection.  Block = (1024-sample time tile, group g); thread = 4 consecutive
+// samples; the group's entries (row, mu, 1/sigma, sign) are staged in shared memory and U streams
+// are loaded per step (U x 16-32 B in flight per thread) before the FP64 accumulation, which runs
+// in ascending input order with explicit _rn operations (no contraction).
 template <typename T>
 __global__ void __launch_bounds__(kProjThreads)
 project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan plan, int mode,
                      double* __restrict__ R64, T* __restrict__ R, bool vec) {
-  constexpr int VN = VecOf<T>::N;
-  constexpr int IT = (sizeof(T) == 4) ? 2 : 4;  // vectors per thread: 8 floats or 8 doubles
-  constexpr int E = VN * IT;                    // samples per thread
+  constexpr int U = 8;
   __shared__ int32_t s_row[kProjBatch];
   __shared__ double s_mu[kProjBatch];
   __shared__ double s_inv[kProjBatch];
@@ -244,22 +233,11 @@ project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan pl
   const int g = blockIdx.y;
   const int32_t e0 = plan.off[g], e1 = plan.off[g + 1];
   if (mode != 0 && e0 == e1) return;  // update of an untouched group: nothing to do
-  const int64_t tile = (int64_t)kProjThreads * E;
-  const int64_t base = (int64_t)blockIdx.x * tile;
-
-  double acc[E];
+  const int64_t e = ((int64_t)blockIdx.x * kProjThreads + threadIdx.x) * 4;
   double* r64 = R64 + (int64_t)g * n;
-  if (mode == 0) {
+  double acc[4];
 #pragma unroll
-    for (int q = 0; q < E; ++q) acc[q] = 0.0;
-  } else {
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
-#pragma unroll
-      for (int q = 0; q < VN; ++q) acc[it * VN + q] = (e + q < n) ? r64[e + q] : 0.0;
-    }
-  }
+  for (int q = 0; q < 4; ++q) acc[q] = (mode != 0 && e + q < n) ? r64[e + q] : 0.0;
 
   for (int32_t b0 = e0; b0 < e1; b0 += kProjBatch) {
     const int nb = min(kProjBatch, e1 - b0);
@@ -272,54 +250,37 @@ project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan pl
     }
     __syncthreads();
     int q0 = 0;
-    constexpr int U = 4;
     for (; q0 + U <= nb; q0 += U) {
-      double x[U][E];
+      Raw4<T> x[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T* row = Tm + (int64_t)s_row[q0 + u] * ld;
-#pragma unroll
-        for (int it = 0; it < IT; ++it) {
-          const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
-          vload<T>(row, &x[u][it * VN], e, n, vec);
-        }
-      }
+      for (int u = 0; u < U; ++u) rload(x[u], Tm + (int64_t)s_row[q0 + u] * ld, e, n, vec);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const double mu = s_mu[q0 + u], inv = s_inv[q0 + u];
         const bool pos = (s_sign[q0 + u] > 0) == (mode >= 0);
 #pragma unroll
-        for (int q = 0; q < E; ++q) {
-          const double z = __dmul_rn(__dsub_rn(x[u][q], mu), inv);
+        for (int q = 0; q < 4; ++q) {
+          const double z = __dmul_rn(__dsub_rn(rget(x[u], q), mu), inv);
           acc[q] = pos ? __dadd_rn(acc[q], z) : __dsub_rn(acc[q], z);
         }
       }
     }
     for (; q0 < nb; ++q0) {
-      double x[E];
-      const T* row = Tm + (int64_t)s_row[q0] * ld;
-#pragma unroll
-      for (int it = 0; it < IT; ++it) {
-        const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
-        vload<T>(row, &x[it * VN], e, n, vec);
-      }
+      Raw4<T> x;
+      rload(x, Tm + (int64_t)s_row[q0] * ld, e, n, vec);
       const double mu = s_mu[q0], inv = s_inv[q0];
       const bool pos = (s_sign[q0] > 0) == (mode >= 0);
 #pragma unroll
-      for (int q = 0; q < E; ++q) {
-        const double z = __dmul_rn(__dsub_rn(x[q], mu), inv);
+      for (int q = 0; q < 4; ++q) {
+        const double z = __dmul_rn(__dsub_rn(rget(x, q), mu), inv);
         acc[q] = pos ? __dadd_rn(acc[q], z) : __dsub_rn(acc[q], z);
       }
     }
   }
-
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const int64_t e = base + ((int64_t)it * kProjThreads + threadIdx.x) * VN;
-#pragma unroll
-    for (int h2 = 0; h2 < VN; h2 += 2)  // FP64 master: VN input samples as double2 stores
-      store_out<double>(r64, e + h2, n, &acc[it * VN + h2]);
-    if ((void*)R != (void*)R64) store_out<T>(R + (int64_t)g * n, e, n, &acc[it * VN]);
+  store_out<double>(r64, e, n, &acc[0]);
+  store_out<double>(r64, e + 2, n, &acc[2]);
+  if ((void*)R != (void*)R64) {
+    if constexpr (sizeof(T) == 4) store_out<float>(reinterpret_cast<float*>(R) + (int64_t)g * n, e, n, acc);
   }
 }
 
@@ -412,13 +373,13 @@ cudaError_t launch_stream_stats(const void* T, int64_t d, int64_t n, int64_t ld,
 cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype, int k,
                                  CsrPlan plan, int mode, double* R64, void* R, cudaStream_t st) {
   if (dtype == SKMP_F32) {
-    const int64_t tile = (int64_t)kProjThreads * 8;
+    const int64_t tile = (int64_t)kProjThreads * 4;
     dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
     const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 4 == 0);
     project_count_kernel<float><<<grid, kProjThreads, 0, st>>>(
         static_cast<const float*>(T), ld, n, plan, mode, R64, static_cast<float*>(R), vec);
   } else {
-    const int64_t tile = (int64_t)kProjThreads * 8;
+    const int64_t tile = (int64_t)kProjThreads * 4;
     dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
     const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 2 == 0);
     project_count_kernel<double><<<grid, kProjThreads, 0, st>>>(

@@ -1,3 +1,5 @@
-python tools/join_bench.py
-SKMP_JOIN_IMPL=x2 python tools/join_bench.py | sed 's/^/x2 /'
-SKMP_JOIN_IMPL=x2 timeout 600 python -m pytest tests/test_gpu_mp.py -q -x 2>&1 | tail -2
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+ARGS="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+python bench.py $ARGS > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches2.csv python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
