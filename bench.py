@@ -188,10 +188,6 @@ def run_reference(args, cfg, top):
 # ----------------------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------------------
-def shard(ids: np.ndarray, rank: int, world: int) -> np.ndarray:
-    return np.array_split(ids, world)[rank]
-
-
 def main():
     args = parse()
     import synthgen
@@ -204,6 +200,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2311_03393_b200 as skmp
+    from paper_2311_03393_b200 import dist as sdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,8 +217,8 @@ def main():
     t_gen = time.perf_counter()
     ids_all = synthgen.stream_ids(cfg)
     add_ids, del_ids = synthgen.dynamic_ids(cfg)
-    my_ids = shard(ids_all, rank, world)
-    my_add = shard(add_ids, rank, world)
+    my_ids = sdist.shard(ids_all, rank, world)
+    my_add = sdist.shard(add_ids, rank, world)
     my_del = np.array([j for j in del_ids if j in set(my_ids.tolist())], dtype=np.uint64)
     host_T = torch.from_numpy(synthgen.streams(cfg, my_ids)).pin_memory()
     host_add = torch.from_numpy(synthgen.streams(cfg, my_add)).pin_memory() if len(my_add) else None
@@ -235,7 +232,7 @@ def main():
         f"add {0 if Tadd is None else Tadd.shape[0]}, del {0 if Tdel is None else Tdel.shape[0]}")
 
     n_sub, excl, m, k = cfg.n_sub, cfg.excl, cfg.m, cfg.k
-    lo, hi = skmp.mp_band(n_sub, excl, dcode, world, rank)
+    lo, hi = sdist.band_for_rank(n_sub, excl, dcode, world, rank)
     cells_total = cfg.cells()
     a0 = max(lo, excl + 1)
     b0 = min(max(hi, a0), n_sub)
@@ -252,8 +249,7 @@ def main():
         if Tdl is not None:
             skmp.sketch_del_dim(sk, Tdl, my_del)
         if world > 1:
-            dist.all_reduce(sk.R64, op=dist.ReduceOp.SUM)
-            skmp.sketch_refresh(sk)
+            sdist.allreduce_sketch(sk)
         if e: e[2].record()
         w = skmp.mp_create(sk.R, m, reseed_rows=args.reseed)
         if e: e[3].record()
@@ -261,17 +257,7 @@ def main():
         if e: e[4].record()
         if world > 1:
             keys, words = skmp.mp_keys(w)
-            if words == 1:
-                dist.all_reduce(keys, op=dist.ReduceOp.MAX)
-            else:  # FP64: lexicographic (value word, then index word among ties)
-                kv = keys.view(-1, 2)
-                v = kv[:, 0].clone()
-                dist.all_reduce(v, op=dist.ReduceOp.MAX)
-                kv[:, 1].masked_fill_(kv[:, 0] != v, torch.iinfo(torch.int64).min)
-                kv[:, 0].copy_(v)
-                col = kv[:, 1].clone()
-                dist.all_reduce(col, op=dist.ReduceOp.MAX)
-                kv[:, 1].copy_(col)
+            sdist.reduce_keys(keys, words)
         res = None
         if rank == 0:
             P, I, inert = skmp.mp_finalize(w)

@@ -1,0 +1,78 @@
+"""Multi-GPU orchestration of the hot path, one process per GPU.
+
+Sketch: streams are sharded over ranks; each rank builds the partial sketch of its shard with
+the shared (seeded, id-keyed) plan, and the FP64 master accumulators are sum-all-reduced
+(linearity of Alg. 1), then re-rounded on every rank (sketch_refresh).
+Join: the diagonals [excl+1, n_sub) are split into equal-cell bands on the tile grid (mp_band);
+each rank joins its band into its own profile keys, which are max-all-reduced (FP32: one signed
+int64 MAX on {orderable rho, ~j}; FP64: MAX on the value word, then MAX on the index word among
+the ranks holding that value), after which any rank can finalize.
+
+Only the collectives live here (torch.distributed: NCCL on GPUs, gloo in the CPU tests);
+every computation step is a C-ABI call into libsketchmp.so.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import torch
+import torch.distributed as dist
+
+from . import (F32, F64, Sketch, mp_band, mp_create, mp_finalize, mp_join, mp_keys, sketch_refresh,
+               sketch_view64)
+
+INT64_MIN = -(1 << 63)
+
+
+def shard(ids, rank: int, world: int):
+    """Contiguous id shard of `rank` (streams are independent, so any split is valid)."""
+    return np.array_split(np.asarray(ids), world)[rank]
+
+
+def band_for_rank(n_sub: int, excl: int, dtype: int, world: int, rank: int) -> tuple[int, int]:
+    return mp_band(n_sub, excl, dtype, world, rank)
+
+
+def allreduce_sketch(sk: Sketch, group=None) -> None:
+    """Sum the per-rank partial FP64 sketches in place and refresh the dtype copy."""
+    R64 = sketch_view64(sk)
+    dist.all_reduce(R64, op=dist.ReduceOp.SUM, group=group)
+    sketch_refresh(sk)
+
+
+def reduce_keys(keys: torch.Tensor, words: int, group=None) -> None:
+    """In-place max-reduce of profile keys across ranks (the NCCL min-with-index reduce of
+    SURVEY §8(e), expressed on the library's larger-is-better key words)."""
+    if words == 1:
+        dist.all_reduce(keys, op=dist.ReduceOp.MAX, group=group)
+        return
+    kv = keys.view(-1, 2)
+    v = kv[:, 0].clone()
+    dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+    idx = kv[:, 1].clone()
+    idx.masked_fill_(kv[:, 0] != v, INT64_MIN)
+    dist.all_reduce(idx, op=dist.ReduceOp.MAX, group=group)
+    kv[:, 0].copy_(v)
+    kv[:, 1].copy_(idx)
+
+
+def mp_selfjoin_dist(R: torch.Tensor, m: int, *, excl: int = -1, reseed_rows: int = 0, group=None,
+                     finalize_on_all: bool = False):
+    """Self-join of R (k x n, replicated on every rank) split into diagonal bands over the ranks
+    of `group`.  Returns (P, I, inert) on rank 0 (and on all ranks if finalize_on_all)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = R.shape[1]
+    n_sub = n - m + 1
+    e = (m + 1) // 2 if excl < 0 else excl
+    dtype = F32 if R.dtype == torch.float32 else F64
+    w = mp_create(R, m, excl=e, reseed_rows=reseed_rows)
+    lo, hi = band_for_rank(n_sub, e, dtype, world, rank)
+    mp_join(w, lo, hi)
+    keys, words = mp_keys(w)
+    reduce_keys(keys, words, group)
+    out = None
+    if rank == 0 or finalize_on_all:
+        out = mp_finalize(w)
+    w.free()
+    return out

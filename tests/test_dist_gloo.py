@@ -1,0 +1,137 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): the diagonal-band partition (mp_band of the
+C-ABI, host-only), the max-reduce of packed profile keys (dist.reduce_keys) and the sum-reduce of
+partial sketches — checked against the oracle computed over the whole problem.  The GPU kernels
+are not involved (they are covered by the -m gpu parity tests, incl. band invariance)."""
+from __future__ import annotations
+
+import math
+import os
+import socket
+import struct
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synthgen
+from oracle import reference as ref
+from oracle.hashplan import plan_count_sketch
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ord32(f: float) -> int:
+    b = struct.unpack("<i", struct.pack("<f", f))[0]
+    return b if b >= 0 else b ^ 0x7FFFFFFF
+
+
+def _ord64(f: float) -> int:
+    b = struct.unpack("<q", struct.pack("<d", f))[0]
+    return b if b >= 0 else b ^ 0x7FFFFFFFFFFFFFFF
+
+
+def _band_keys(r, m, excl, lo, hi, words):
+    """Oracle keys of one diagonal band: for every row i the best rho over j with |i-j| in
+    [max(lo, excl+1), hi), packed like the library's keys (larger is better)."""
+    Z, flat = ref.znorm_windows(r, m)
+    n_sub = Z.shape[0]
+    keys = np.full((n_sub, words), np.iinfo(np.int64).min, dtype=np.int64)
+    a = max(lo, excl + 1)
+    for i in range(n_sub):
+        best = None
+        for j in range(n_sub):
+            dd = abs(i - j)
+            if dd < a or dd >= hi:
+                continue
+            rho = 1.0 - float(((Z[i] - Z[j]) ** 2).sum()) / (2 * m)
+            if best is None or rho > best[0] or (rho == best[0] and j < best[1]):
+                best = (rho, j)
+        if best is None:
+            continue
+        rho, j = best
+        if words == 1:
+            v = (_ord32(float(np.float32(rho))) << 32) | (0xFFFFFFFF - j)
+            keys[i, 0] = v if v < (1 << 63) else v - (1 << 64)
+        else:
+            keys[i, 0] = _ord64(rho)
+            keys[i, 1] = -1 - j
+    return keys
+
+
+def _worker(rank, world, port, q):
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        import paper_2311_03393_b200 as skmp
+        from paper_2311_03393_b200 import dist as sdist
+        out = {}
+        # ---- join: bands + key reduce ----------------------------------------------------
+        r = synthgen.mp_series(1, 420, seed=11, kind="mix")[0]
+        m = 16
+        excl = 8
+        n_sub = len(r) - m + 1
+        for dtype, words in ((skmp.F32, 1), (skmp.F64, 2)):
+            lo, hi = sdist.band_for_rank(n_sub, excl, dtype, world, rank)
+            k = torch.from_numpy(_band_keys(r, m, excl, lo, hi, words).reshape(-1).copy())
+            sdist.reduce_keys(k, words)
+            out[f"keys{words}"] = k.numpy().reshape(n_sub, words)
+            out[f"band{words}"] = (lo, hi)
+        # ---- sketch: shard streams, sum partial sketches ---------------------------------
+        cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=600, k=3)
+        ids = np.arange(cfg.d)
+        mine = sdist.shard(ids, rank, world)
+        T = synthgen.streams(cfg, mine)
+        g, s = plan_count_sketch(mine, cfg.k, cfg.seed)
+        Rp, _, _ = ref.sketch(T, cfg.k, g, s)
+        Rt = torch.from_numpy(Rp.copy())
+        dist.all_reduce(Rt, op=dist.ReduceOp.SUM)
+        out["sketch"] = Rt.numpy()
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_bands_and_reductions():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(rk, world, port, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r = synthgen.mp_series(1, 420, seed=11, kind="mix")[0]
+    m, excl = 16, 8
+    P, I, _ = ref.selfjoin_brute(r, m, excl)
+    for words in (1, 2):
+        # the two bands tile [0, n_sub) on the tile grid
+        b0, b1 = res[0][f"band{words}"], res[1][f"band{words}"]
+        assert b0[0] == 0 and b0[1] == b1[0] and b1[1] == len(P)
+        for rank in range(world):
+            keys = res[rank][f"keys{words}"]
+            if words == 1:
+                j = 0xFFFFFFFF - (keys[:, 0] & 0xFFFFFFFF)
+            else:
+                j = -1 - keys[:, 1]
+            Z, _ = ref.znorm_windows(r, m)
+            for i in range(len(P)):
+                if j[i] != I[i]:  # only a tie at the key's precision is acceptable
+                    d = math.sqrt(((Z[i] - Z[j[i]]) ** 2).sum())
+                    assert abs(d - P[i]) <= (1e-6 if words == 1 else 1e-12) * max(P[i], 1.0), (i, j[i], I[i])
+    cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=600, k=3)
+    T = synthgen.streams(cfg)
+    g, s = plan_count_sketch(np.arange(cfg.d), cfg.k, cfg.seed)
+    R, _, _ = ref.sketch(T, cfg.k, g, s)
+    for rank in range(world):
+        np.testing.assert_allclose(res[rank]["sketch"], R, atol=1e-12)

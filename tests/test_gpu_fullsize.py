@@ -1,0 +1,164 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times, on sampled
+outputs the oracle computes one by one (SURVEY §8(c) "Parity contract"):
+
+* C3 (d=1000, n=1e5, FP32): sketch at sampled time columns; profile at sampled rows of every
+  series; every reported discord's score re-derived by the oracle;
+* C4 (d=10,000, n=2e5, FP32) dynamic test: build, add 500, delete 500 (the bench step) -> the
+  sketch at sampled columns equals the oracle's sketch of the final stream set; sampled rows;
+* C5-shaped join (k=32, n=2e6, m=256, FP32): sampled rows, and bit-identical keys for a 2-band
+  split (the multi-GPU decomposition).
+The oracle always works on its own sketch of the generator's streams (never on GPU output)."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import synthgen
+from oracle import reference as ref
+from oracle.hashplan import plan_count_sketch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _oracle_stats(T):
+    """Two-pass FP64 stream statistics (oracle.stream_stats), vectorised over rows for speed."""
+    mu = np.empty(T.shape[0])
+    sg = np.empty(T.shape[0])
+    for j0 in range(0, T.shape[0], 256):
+        blk = T[j0:j0 + 256].astype(np.float64)
+        m = blk.sum(axis=1) / blk.shape[1]
+        mu[j0:j0 + 256] = m
+        sg[j0:j0 + 256] = np.sqrt(((blk - m[:, None]) ** 2).sum(axis=1) / blk.shape[1])
+    return mu, sg
+
+
+def _sketch_cols(T, mu, sg, groups, signs, k, cols):
+    """Alg. 1 restricted to time columns `cols` (sequential ascending-j sums per group)."""
+    R = np.zeros((k, len(cols)))
+    B = np.zeros((k, len(cols)))
+    X = T[:, cols].astype(np.float64)
+    for j in range(T.shape[0]):
+        z = (X[j] - mu[j]) / sg[j]
+        R[groups[j]] = R[groups[j]] + signs[j] * z
+        B[groups[j]] += np.abs(z)
+    return R, B
+
+
+def _oracle_sketch_full(T, mu, sg, groups, signs, k):
+    R = np.zeros((k, T.shape[1]))
+    for j in range(T.shape[0]):
+        R[groups[j]] += signs[j] * ((T[j].astype(np.float64) - mu[j]) / sg[j])
+    return R
+
+
+def _check_rows(R_or, P, I, m, rows_per_series, seed, tol=1e-3, extra_rows=None):
+    rng = np.random.default_rng(seed)
+    k, n_sub = P.shape
+    excl = (m + 1) // 2
+    for g in range(k):
+        rows = rng.choice(n_sub, size=rows_per_series, replace=False)
+        if extra_rows is not None and g in extra_rows:
+            rows = np.unique(np.concatenate([rows, extra_rows[g]]))
+        Po, Io, Fo = ref.selfjoin_rows(R_or[g], m, excl, rows=rows)
+        floor = 1e-3 * math.sqrt(m)
+        err = np.abs(P[g, rows] - Po) / np.maximum(Po, floor)
+        assert err.max() <= tol, f"g={g}: rel err {err.max():.2e} at row {rows[int(np.argmax(err))]}"
+        for q, i in enumerate(rows):
+            j = int(I[g, i])
+            assert abs(int(i) - j) > excl
+            if j != Io[q]:  # documented tie: the GPU's neighbour is (within tol) as near
+                d = ref.dist(R_or[g, i:i + m], R_or[g, j:j + m])
+                assert d <= Po[q] * (1 + tol) + floor * tol, (g, i, j, Io[q], d, Po[q])
+
+
+def test_c3_full(cuda):
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.CONFIGS["c3"]
+    T = synthgen.streams(cfg)
+    ids = synthgen.stream_ids(cfg)
+    sk = skmp.sketch_build(torch.from_numpy(T).to(cuda), ids, cfg.k, seed=cfg.seed)
+    P, I, inert = skmp.mp_selfjoin(sk.R, cfg.m)
+    top = skmp.discord_topk(P, I, inert, m=cfg.m, top=20)
+    torch.cuda.synchronize()
+    g, s = plan_count_sketch(ids, cfg.k, cfg.seed)
+    mu, sg = _oracle_stats(T)
+    cols = np.random.default_rng(3).choice(cfg.n, 64, replace=False)
+    Rc, B = _sketch_cols(T, mu, sg, g, s, cfg.k, cols)
+    R64 = sk.R64.cpu().numpy()
+    assert np.all(np.abs(R64[:, cols] - Rc) <= 1e-12 * B)
+    R_or = _oracle_sketch_full(T, mu, sg, g, s, cfg.k)
+    Pn, In = P.cpu().numpy(), I.cpu().numpy()
+    extra = {}
+    for d in top:
+        extra.setdefault(d.g, []).append(d.t)
+    _check_rows(R_or, Pn, In, cfg.m, 3, seed=33, extra_rows={k_: np.array(v) for k_, v in extra.items()})
+    for d in top:  # reported scores are the profile values, and the oracle agrees
+        assert d.score == float(Pn[d.g, d.t])
+        assert d.score == max(float(Pn[gg, d.t]) for gg in range(cfg.k) if not inert[gg])
+    hits = sum(1 for q in synthgen.injections(cfg) if any(abs(d.t - q.t) < cfg.m for d in top))
+    print(f"C3: {hits}/{len(synthgen.injections(cfg))} injected discords within the top-20")
+
+
+def test_c4_dynamic_full(cuda):
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.CONFIGS["c4"]
+    ids = synthgen.stream_ids(cfg)
+    add_ids, del_ids = synthgen.dynamic_ids(cfg)
+    T = synthgen.streams(cfg)
+    Ta = synthgen.streams(cfg, add_ids)
+    Td = torch.from_numpy(T).to(cuda)
+    sk = skmp.sketch_build(Td, ids, cfg.k, seed=cfg.seed)
+    skmp.sketch_add_dim(sk, torch.from_numpy(Ta).to(cuda), add_ids)
+    skmp.sketch_del_dim(sk, Td[del_ids.astype(np.int64)].contiguous(), del_ids)
+    P, I, inert = skmp.mp_selfjoin(sk.R, cfg.m)
+    torch.cuda.synchronize()
+    keep = np.setdiff1d(np.arange(cfg.d), del_ids.astype(np.int64))
+    final_T = np.concatenate([T[keep], Ta])
+    final_ids = np.concatenate([ids[keep], add_ids])
+    del T, Td
+    g, s = plan_count_sketch(final_ids, cfg.k, cfg.seed)
+    mu, sg = _oracle_stats(final_T)
+    cols = np.random.default_rng(4).choice(cfg.n, 32, replace=False)
+    Rc, B = _sketch_cols(final_T, mu, sg, g, s, cfg.k, cols)
+    R64 = sk.R64.cpu().numpy()
+    assert np.all(np.abs(R64[:, cols] - Rc) <= 1e-12 * B)
+    plan = skmp.sketch_plan(sk)
+    assert sorted(plan["ids"].tolist()) == sorted(final_ids.tolist())
+    R_or = _oracle_sketch_full(final_T, mu, sg, g, s, cfg.k)
+    _check_rows(R_or, P.cpu().numpy(), I.cpu().numpy(), cfg.m, 1, seed=44)
+
+
+def test_c5_shape_join_and_bands(cuda):
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.CONFIGS["c5"]
+    k, n, m = cfg.k, cfg.n, cfg.m
+    R = synthgen.mp_series_torch(k, n, cfg.seed, cuda, torch.float32)
+    Rh = R.double().cpu().numpy()  # generator output (input plumbing), not a CUDA-path result
+    w = skmp.mp_create(R, m)
+    n_sub, excl = n - m + 1, (m + 1) // 2
+    for b in range(2):
+        lo, hi = skmp.mp_band(n_sub, excl, skmp.F32, 2, b)
+        skmp.mp_join(w, lo, hi)
+    keys2, _ = skmp.mp_keys(w)
+    keys2 = keys2.clone()
+    P, I, _ = skmp.mp_finalize(w)
+    w.free()
+    w1 = skmp.mp_create(R, m)
+    skmp.mp_join(w1)
+    keys1, _ = skmp.mp_keys(w1)
+    torch.cuda.synchronize()
+    assert torch.equal(keys1, keys2), "2-band split changed the keys"
+    w1.free()
+    # sampled rows of a few series (C5 rows cost ~1 core-second each in the oracle)
+    rng = np.random.default_rng(5)
+    Pn, In = P.cpu().numpy(), I.cpu().numpy()
+    for g in rng.choice(k, 4, replace=False):
+        rows = rng.choice(n_sub, 4, replace=False)
+        Po, Io, _ = ref.selfjoin_rows(Rh[g], m, excl, rows=rows)
+        err = np.abs(Pn[g, rows] - Po) / np.maximum(Po, 1e-3 * math.sqrt(m))
+        assert err.max() <= 1e-3, err
