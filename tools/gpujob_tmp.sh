@@ -1,5 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
-ARGS="--steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
-python bench.py $ARGS > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches2.csv python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x -s --durations=5 > gpurun_out/fullsize.log 2>&1; echo rc=$?; tail -15 gpurun_out/fullsize.log
