@@ -565,7 +565,20 @@ skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t d
   w.excl = excl;
   w.n_sub = n - cfg->m + 1;
   w.ldq = round_up(w.n_sub + join_pad(dtype), 64);
-  const int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 8192 : 2048);
+  int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 8192 : 2048);
+  if (cfg->reseed_rows <= 0) {
+    // small problems: shorten the tiles until the grid has ~2 waves of 148 SMs x 16 warps
+    const int64_t W = join_width(dtype);
+    auto tiles = [&](int64_t L) {
+      int64_t t = 0;
+      for (int64_t d0 = ((excl + 1) / W) * W; d0 < w.n_sub; d0 += W) {
+        const int64_t rows = w.n_sub - (d0 > excl + 1 ? d0 : excl + 1);
+        t += (rows + L - 1) / L;
+      }
+      return t * k;
+    };
+    while (L0 > 256 && tiles(L0) < 2 * 148 * 16) L0 /= 2;
+  }
   w.L = (int)round_up(L0, 64);
   w.R = R;
   const int words = dtype == SKMP_F32 ? 1 : 2;

@@ -1,1 +1,5 @@
-timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x -s --durations=5 > gpurun_out/fullsize.log 2>&1; echo rc=$?; tail -15 gpurun_out/fullsize.log
+python tools/join_bench.py --dtype f64 --k 16 --n 20000 --m 100 | sed "s/^/c2 /"
+python tools/join_bench.py --dtype f32 --k 16 --n 20000 --m 100 | sed "s/^/c2f32 /"
+python tools/join_bench.py --dtype f64 --k 4 --n 2000 --m 50 | sed "s/^/c1 /"
+python tools/join_bench.py --dtype f32 --k 32 --n 100000 --m 128 | sed "s/^/c3 /"
+python tools/join_bench.py
