@@ -43,7 +43,12 @@ constexpr int kJoinD64 = 8;
 #endif
 constexpr int kJoinC = SKMP_JOIN_C;  // rows per staged chunk (power of two, multiple of 2D)
 int join_d32();                // diagonals per thread of the FP32 join (env SKMP_JOIN_D: 8 | 16)
-inline int join_width(int dtype) { return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : join_d32()); }
+bool join_x2_enabled();        // packed f32x2 FP32 join selected (SKMP_JOIN_IMPL=x2)
+int join_x2_width();           // its tile width
+inline int join_width(int dtype) {
+  if (dtype == SKMP_F32 && join_x2_enabled()) return join_x2_width();
+  return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : join_d32());
+}
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
 inline int64_t join_pad(int dtype) { return join_width(dtype) + 4 * kJoinC + 64; }
 
@@ -103,7 +108,6 @@ cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
 cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
 // packed f32x2 FP32 join (mp_join_x2.cu), opt-in with SKMP_JOIN_IMPL=x2
-bool join_x2_enabled();
 cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
                               int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
 cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);

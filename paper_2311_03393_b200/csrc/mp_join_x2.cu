@@ -28,7 +28,12 @@ namespace {
 using namespace join;
 
 constexpr int NT = 32;            // one warp per CTA
-constexpr int DG = 4;             // diagonals per group per thread
+#ifndef SKMP_X2_DG
+#define SKMP_X2_DG 8
+#endif
+constexpr int DG = SKMP_X2_DG;    // diagonals per group per thread (2 DG cells per row)
+constexpr unsigned KMUL = 2 * DG; // key multiplier: room for the 2*DG slot codes
+constexpr unsigned KADD = 0u - 0x3F800000u * KMUL;  // (bits(y) - bits(1.0)) * KMUL, mod 2^32
 constexpr int H = NT * DG;        // 128: group B offset; tile width W = 2H
 constexpr int W = 2 * H;
 constexpr int C = kJoinC;         // rows per staged chunk
@@ -64,11 +69,11 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
   return d;
 }
 
-// key of one cell: y = rho + 2 in [1, 4); key = (bits(y) - bits(1.0)) * 8 + code  (IMAD, FMA pipe)
+// key of one cell: y = rho + 2 in [1, 4); key = (bits(y) - bits(1.0)) * KMUL + code (IMAD, FMA pipe)
 template <int code>
-__device__ __forceinline__ float key_of(float y, unsigned eight) {
+__device__ __forceinline__ float key_of(float y, unsigned kmul) {
   unsigned k;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(eight), "n"(0x04000000 + code));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(kmul), "n"(KADD + code));
   return __uint_as_float(k);
 }
 
@@ -112,7 +117,7 @@ __device__ __noinline__ void publish_x2(int64_t* keys, Smem* sm, int rbu, int ct
                                         int64_t i_u, int64_t dt, float rowa, float rowb,
                                         float cA0, float cA1, float cB0, float cB1) {
   auto jrow = [&](float v, int64_t i) {
-    const int s = __float_as_int(v) & 7;
+    const int s = __float_as_int(v) & (2 * DG - 1);
     return i + dt + (s & (DG - 1)) + (s >= DG ? H : 0);
   };
   if (rowa > sm->rthr[rbu]) {
@@ -126,22 +131,22 @@ __device__ __noinline__ void publish_x2(int64_t* keys, Smem* sm, int rbu, int ct
   // group A column c = i + dt (completes after row i): its cells have codes d = c - i' - dt
   if (cA0 > sm->thrA[ctA0]) {
     const int64_t c = i_u + dt;
-    publish(keys, c, cA0, c - dt - (__float_as_int(cA0) & 7));
+    publish(keys, c, cA0, c - dt - (__float_as_int(cA0) & (2 * DG - 1)));
     sm->thrA[ctA0] = cA0;
   }
   if (cA1 > sm->thrA[ctA1]) {
     const int64_t c = i_u + 1 + dt;
-    publish(keys, c, cA1, c - dt - (__float_as_int(cA1) & 7));
+    publish(keys, c, cA1, c - dt - (__float_as_int(cA1) & (2 * DG - 1)));
     sm->thrA[ctA1] = cA1;
   }
   if (cB0 > sm->thrB[ctA0]) {
     const int64_t c = i_u + dt + H;
-    publish(keys, c, cB0, c - dt - H - ((__float_as_int(cB0) & 7) - DG));
+    publish(keys, c, cB0, c - dt - H - ((__float_as_int(cB0) & (2 * DG - 1)) - DG));
     sm->thrB[ctA0] = cB0;
   }
   if (cB1 > sm->thrB[ctA1]) {
     const int64_t c = i_u + 1 + dt + H;
-    publish(keys, c, cB1, c - dt - H - ((__float_as_int(cB1) & 7) - DG));
+    publish(keys, c, cB1, c - dt - H - ((__float_as_int(cB1) & (2 * DG - 1)) - DG));
     sm->thrB[ctA1] = cB1;
   }
 }
@@ -270,7 +275,10 @@ __device__ __forceinline__ void land_row(const RowStage& s, Smem* sm, int64_t i)
   sm->rthr[e] = s.t;
 }
 
-__global__ void __launch_bounds__(NT)
+#ifndef SKMP_X2_MINB
+#define SKMP_X2_MINB 1
+#endif
+__global__ void __launch_bounds__(NT, SKMP_X2_MINB)
 join_x2_kernel(JoinArgs a) {
   __shared__ Smem sm;
   __shared__ int64_t s_tile[3];
@@ -384,13 +392,15 @@ join_x2_kernel(JoinArgs a) {
   for (int x = 0; x < DG - 1; ++x) {
     const int64_t c = i1 + dt + x;
     const int e = pos(c);
-    if (c < n_sub && CA[x] > sm.thrA[e]) publish(keys, c, CA[x], c - dt - (__float_as_int(CA[x]) & 7));
+    if (c < n_sub && CA[x] > sm.thrA[e]) publish(keys, c, CA[x], c - dt - (__float_as_int(CA[x]) & (2 * DG - 1)));
     if (c + H < n_sub && CB[x] > sm.thrB[e])
-      publish(keys, c + H, CB[x], c - dt - ((__float_as_int(CB[x]) & 7) - DG));
+      publish(keys, c + H, CB[x], c - dt - ((__float_as_int(CB[x]) & (2 * DG - 1)) - DG));
   }
 }
 
 }  // namespace
+
+int join_x2_width() { return W; }
 
 bool join_x2_enabled() {
   static const bool on = [] {
@@ -418,7 +428,7 @@ cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const in
   a.prefix = prefix;
   a.nblk = nblk;
   a.blk0 = blk0;
-  a.eight = 8;
+  a.eight = KMUL;
   dim3 grid((unsigned)ntiles, (unsigned)w.k);
   join_x2_kernel<<<grid, NT, 0, st>>>(a);
   count_launches(1);
