@@ -220,13 +220,22 @@ def main():
     my_ids = sdist.shard(ids_all, rank, world)
     my_add = sdist.shard(add_ids, rank, world)
     my_del = np.array([j for j in del_ids if j in set(my_ids.tolist())], dtype=np.uint64)
-    host_T = torch.from_numpy(synthgen.streams(cfg, my_ids)).pin_memory()
-    host_add = torch.from_numpy(synthgen.streams(cfg, my_add)).pin_memory() if len(my_add) else None
     pos = {int(j): q for q, j in enumerate(my_ids)}
-    host_del = host_T[[pos[int(j)] for j in my_del]].contiguous().pin_memory() if len(my_del) else None
-    Td = host_T.to(dev, non_blocking=False)
-    Tadd = host_add.to(dev) if host_add is not None else None
-    Tdel = host_del.to(dev) if host_del is not None else None
+    big = cfg.d * cfg.n >= 2_000_000_000 // world and cfg.kind == "seasonal_noise"
+    if big:
+        # C5 (16 GB): numpy would cost minutes of host time; same recipe family on the device
+        # (synthgen.streams_torch, Philox), host copy only for the e2e leg
+        Td = synthgen.streams_torch(cfg, dev, my_ids)
+        Tadd = synthgen.streams_torch(cfg, dev, my_add) if len(my_add) else None
+        Tdel = Td[[pos[int(j)] for j in my_del]].contiguous() if len(my_del) else None
+        host_T = host_add = host_del = None
+    else:
+        host_T = torch.from_numpy(synthgen.streams(cfg, my_ids)).pin_memory()
+        host_add = torch.from_numpy(synthgen.streams(cfg, my_add)).pin_memory() if len(my_add) else None
+        host_del = host_T[[pos[int(j)] for j in my_del]].contiguous().pin_memory() if len(my_del) else None
+        Td = host_T.to(dev, non_blocking=False)
+        Tadd = host_add.to(dev) if host_add is not None else None
+        Tdel = host_del.to(dev) if host_del is not None else None
     torch.cuda.synchronize()
     log(f"[rank {rank}] inputs ready in {time.perf_counter() - t_gen:.1f}s: T {tuple(Td.shape)}, "
         f"add {0 if Tadd is None else Tadd.shape[0]}, del {0 if Tdel is None else Tdel.shape[0]}")
@@ -310,7 +319,14 @@ def main():
 
     # ---------------- e2e: host (pinned) inputs through the C-ABI ----------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and host_T is None:
+        try:  # pinned host copies of the device-generated inputs (needs ~d*n*4 bytes of host RAM)
+            host_T = Td.cpu().pin_memory()
+            host_add = Tadd.cpu().pin_memory() if Tadd is not None else None
+            host_del = Tdel.cpu().pin_memory() if Tdel is not None else None
+        except RuntimeError as ex:
+            log(f"[rank {rank}] e2e skipped: {ex}")
+    if not args.no_e2e and host_T is not None:
         step(host_T, host_add, host_del)  # warm the staging pool
         barrier()
         s0, s1 = ev(), ev()

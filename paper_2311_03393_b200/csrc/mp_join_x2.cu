@@ -70,10 +70,17 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
 }
 
 // key of one cell: y = rho + 2 in [1, 4); key = (bits(y) - bits(1.0)) * KMUL + code (IMAD, FMA pipe)
+#ifndef SKMP_X2_LEA_B
+#define SKMP_X2_LEA_B 0  // 1: group-B keys use an ALU shift-add (LEA) instead of the FMA-pipe IMAD
+#endif
 template <int code>
 __device__ __forceinline__ float key_of(float y, unsigned kmul) {
   unsigned k;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(kmul), "n"(KADD + code));
+  if constexpr (SKMP_X2_LEA_B && code >= DG) {
+    k = __float_as_uint(y) * KMUL + (KADD + code);
+  } else {
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(kmul), "n"(KADD + code));
+  }
   return __uint_as_float(k);
 }
 
