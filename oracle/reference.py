@@ -16,6 +16,8 @@ Function pins (tests/test_oracle_pins.py):
   selfjoin_rows (C)          -> selfjoin_brute on tiny inputs
   combine / topk_greedy      -> an independent sort-then-scan reimplementation
   detect (identity plan)     -> per-stream exact profiles of Def. 5
+  dimension_detection        -> scipy cdist distance profile; exact repeat (periodic stream)
+                                -> score 0; planted single-stream burst -> j* on it
 """
 from __future__ import annotations
 
@@ -239,3 +241,45 @@ def detect(T: np.ndarray, k: int, m: int, K: int, *, groups=None, signs=None, S=
     C, G = combine(P, inert)
     top = topk_greedy(C, G, I, K, radius)
     return dict(R=R, mu=mu, sigma=sigma, P=P, I=I, flat=np.stack(Fs), inert=inert, C=C, G=G, top=top)
+
+
+# ------------------------------------------------------------------------------------------
+# f2: Alg. 3 Dimension-Detection in the single-series mode of P:L322,
+# and the optional refinement join on j*
+# ------------------------------------------------------------------------------------------
+
+def dimension_detection(T: np.ndarray, rows, t_star: int, m: int, excl: int | None = None):
+    """Alg. 3 with the self-join variant: for every stream j of J_{g*} (given as the
+    rows of T, in the group's order) s^(j) = 1NN_dist(T_{j, t*, m}, T_j) (Def. 4/6: the nearest
+    admissible window |t - t*| > excl, reading 7; smallest t on ties, reading 8; flat
+    convention reading 5 on the stream as given), then j* = the first strict maximiser
+    (lines 3-7; starting from -inf instead of s_bsf = 0 so an all-zero group still names its
+    first member, reading 20).  Returns (scores, nn, j_star) with j_star an index into rows."""
+    T = np.asarray(T, dtype=np.float64)
+    excl = (m + 1) // 2 if excl is None else excl
+    scores = np.empty(len(rows))
+    nns = np.empty(len(rows), dtype=np.int64)
+    for q, j in enumerate(rows):
+        Z, flat = znorm_windows(T[j], m)
+        n_sub = Z.shape[0]
+        diff = Z - Z[t_star][None, :]
+        d2 = (diff * diff).sum(axis=1)
+        d2 = np.where(flat & flat[t_star], 0.0, np.where(flat ^ flat[t_star], float(m), d2))
+        adm = np.abs(np.arange(n_sub) - t_star) > excl
+        d2 = np.where(adm, d2, np.inf)
+        t = int(np.argmin(d2))                          # first occurrence = smallest t
+        nns[q] = t
+        scores[q] = math.sqrt(d2[t])
+    best, j_star = -np.inf, -1
+    for q in range(len(rows)):                          # Alg. 3 line 5: strict '>' in J_g* order
+        if scores[q] > best:
+            best, j_star = scores[q], q
+    return scores, nns, j_star
+
+
+def refine(r: np.ndarray, m: int, excl: int | None = None):
+    """Refinement: the full self-join profile of the identified stream and its
+    top-1 discord (smallest-index argmax, reading 8).  Returns (t, nn, score, P, I)."""
+    P, I, _ = selfjoin_rows(r, m, excl)
+    t = int(np.argmax(P))
+    return t, int(I[t]), float(P[t]), P, I

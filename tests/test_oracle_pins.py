@@ -278,3 +278,43 @@ def test_injected_discord_recovery():
     P0, I0, _ = ref.selfjoin_rows(T[0], cfg.m)
     top = ref.topk_greedy(P0, np.zeros(len(P0), int), I0[None], 3, cfg.excl)
     assert any(1200 - cfg.m < tt < 1250 for tt, *_ in top), top
+
+
+# ---------------------------------------------------------------------------------- Alg. 3
+def test_dimension_detection_vs_cdist_and_planted():
+    """Alg. 3 (self-join mode P:L322): per-stream 1NN distance of window t* pinned to
+    scipy cdist; an exactly periodic stream scores 0 (its window repeats one period later); a
+    burst planted in one stream of the group makes that stream j*."""
+    m, n = 32, 900
+    rng = np.random.default_rng(21)
+    t = np.arange(n)
+    T = np.stack([np.sin(2 * np.pi * t / p) + 0.05 * rng.standard_normal(n) for p in (60, 75, 90, 110)])
+    T = np.concatenate([T, np.sin(2 * np.pi * t / 50)[None, :]])   # exact period 50
+    t_star = 400
+    T[2, t_star:t_star + m] += 3.0 * np.sin(2 * np.pi * np.arange(m) / 7)   # burst in stream 2
+    rows = [4, 0, 2, 3, 1]
+    excl = (m + 1) // 2
+    scores, nn, js = ref.dimension_detection(T, rows, t_star, m, excl)
+    for q, j in enumerate(rows):
+        Z, _ = ref.znorm_windows(T[j], m)
+        D = cdist(Z[t_star][None, :], Z)[0]                     # library Euclidean distances
+        D[np.abs(np.arange(len(D)) - t_star) <= excl] = np.inf
+        assert abs(scores[q] - D.min()) < 1e-12 and nn[q] == int(np.argmin(D))
+    assert scores[0] < 1e-6 and (t_star - nn[0]) % 50 == 0     # an exact repeat, whole periods away
+    assert rows[js] == 2                                        # the planted stream
+    # Alg. 3's strict '>' in group order: equal scores keep the first member
+    T2 = np.stack([T[1], T[1], T[3]])
+    s2, _, j2 = ref.dimension_detection(T2, [0, 1, 2], t_star, m, excl)
+    assert s2[0] == s2[1]
+    assert j2 == (0 if s2[0] >= s2[2] else 2)
+
+
+def test_refine_is_top1_of_the_stream_profile():
+    """Refinement: the top-1 discord of the identified stream's full profile,
+    against the cdist profile."""
+    r = synthgen.mp_series(1, 700, seed=23, kind="seasonal")[0]
+    m = 24
+    excl = (m + 1) // 2
+    t, nn, score, P, I = ref.refine(r, m, excl)
+    Pc, Ic = _cdist_profile(r, m, excl)
+    assert t == int(np.argmax(Pc)) and abs(score - Pc.max()) < 1e-12 and nn == Ic[t]
