@@ -168,9 +168,12 @@ skmp_status mp_join(skmp_mp* w, int64_t diag_lo, int64_t diag_hi, void* stream);
 
 /* Device view of the profile keys, for a cross-GPU max-reduce (multi-GPU bands):
  *   keys [dev] count int64 words, `words` per profile entry (FP32: 1, FP64: 2);
- * FP32 word = (orderable(rho_f32) << 32) | (0xFFFFFFFF - j); FP64 words = {orderable(rho_f64),
- * -1 - j}.  Larger is better (max rho, then smallest j): FP32 keys reduce with one signed int64
- * MAX; FP64 keys reduce lexicographically (MAX of word 0, then MAX of word 1 among ties). */
+ * b = the smallest index of the winning candidate set (the D cells one join thread saw for this
+ * entry: D consecutive neighbours [b, b+D), b >= -(D-1); mp_finalize resolves the set exactly);
+ * FP32 word = (orderable(rho_f32) << 32) | (0xFFFFFFFF - (b + 32)); FP64 words =
+ * {orderable(rho_f64), -1 - b}.  Larger is better (max rho, then smallest b): FP32 keys reduce
+ * with one signed int64 MAX; FP64 keys reduce lexicographically (MAX of word 0, then MAX of
+ * word 1 among ties). */
 skmp_status mp_keys(skmp_mp* w, void** keys, int64_t* count, int32_t* words);
 
 /* Host-only: diagonal band `band` of `nbands` equal-cell bands of [excl+1, n_sub), edges
@@ -184,6 +187,8 @@ skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, 
 int32_t mp_tile_width(int32_t dtype);
 
 /* Finalize: keys -> P [dev] k x n_sub (dtype) and I [dev] k x n_sub (int64), inert [host] k.
+ * Each entry's winning candidate set is resolved in FP64 (nearest admissible member, smallest
+ * index on ties) and its distance recomputed from Def. 3 by explicit differences.
  * Requires the full diagonal range to have been joined.  Synchronous only for the inert copy.
  * Errors: INVALID_ARG, CUDA. */
 skmp_status mp_finalize(skmp_mp* w, void* P, int64_t* I, uint8_t* inert, void* stream);
@@ -207,6 +212,28 @@ skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, 
                          int64_t n_sub, int64_t ldp, int32_t m, int32_t dtype, int32_t top,
                          int32_t radius, int64_t* t_out, int32_t* g_out, int64_t* nn_out,
                          double* score_out, int32_t* n_found, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Discord dimension recovery: Alg. 3 Dimension-Detection in the
+ * single-series mode of P:L322 (the same series as train and test, self-join variant):
+ *
+ *   s^(j) = min_{t : |t - t_star| > excl} dist(T_{j, t_star, m}, T_{j, t, m}),  nn^(j) = argmin
+ *
+ * for each listed stream j of the discord's group J_{g*} (dist = z-normalised Euclidean, Def. 3
+ * P:L129-133, evaluated by explicit differences in FP64; flat windows per reading 5 relative
+ * to max|T_j|; smallest t on ties), and j* = the FIRST strict maximiser in the listed order
+ * (Alg. 3 lines 3-7, reading 20).  The refinement join of P:L303-304 is mp_selfjoin on row j*.
+ *   T       [dev|host] (max(rows)+1) x ld streams (dtype), n samples each.
+ *   rows    [host] nrows stream rows of T (the members of J_{g*}, in group order).
+ *   t_star  the discord time from discord_topk, 0 <= t_star < n - m + 1.
+ *   excl    exclusion radius; < 0 -> ceil(m/2) (reading 7).
+ *   scores  [host, out] nrows 1NN distances;  nn [host, out] nrows neighbour times (may be NULL).
+ *   j_star  [host, out] index into rows of the winner.
+ * Synchronous.  Errors: INVALID_ARG (NULL, nrows < 1, bad t_star, m < 2, negative row),
+ * SERIES_TOO_SHORT (n < m), NO_ADMISSIBLE (no window farther than excl from t_star), CUDA, OOM. */
+skmp_status discord_dims(const void* T, int64_t ld, int64_t n, int32_t dtype, const int64_t* rows,
+                         int64_t nrows, int64_t t_star, int32_t m, int32_t excl, double* scores,
+                         int64_t* nn, int64_t* j_star, void* stream);
 
 #ifdef __cplusplus
 }

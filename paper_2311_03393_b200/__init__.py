@@ -5,7 +5,7 @@ PyTorch supplies device memory and the current CUDA stream.  The same names as t
 
     sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
     sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
-    mp_selfjoin, discord_topk
+    mp_selfjoin, discord_topk, discord_dims
 
 There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
 without a GPU return SKMP_E_CUDA (raised as SkmpError).
@@ -83,6 +83,7 @@ _SIGS = {
     "mp_selfjoin": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
     "discord_topk": (ctypes.c_int, [_P, _P, _P, _I32, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
                                     _P, _P]),
+    "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
 }
 
 
@@ -272,6 +273,15 @@ def sketch_plan(sk: Sketch):
     return dict(ids=ids, groups=g, signs=s, mu=mu, sigma=sg)
 
 
+def group_rows(sk: Sketch, g: int) -> np.ndarray:
+    """Plan positions (rows of the sketched T, in input order) of group J_g (Alg. 3's input);
+    every position for a dense projection, whose groups are not disjoint."""
+    pl = sketch_plan(sk)
+    if np.all(pl["groups"] < 0):
+        return np.arange(len(pl["groups"]), dtype=np.int64)
+    return np.nonzero(pl["groups"] == g)[0].astype(np.int64)
+
+
 def sketch_refresh(sk: Sketch, stream=None):
     _check(lib().sketch_refresh(sk.handle, _stream(stream)))
 
@@ -395,3 +405,18 @@ def discord_topk(P, I, inert, m: int, top: int, radius: int = -1, stream=None) -
     _check(lib().discord_topk(_ptr(P), _ptr(I), _ptr(inert_a), k, n_sub, P.stride(0), m, _dtype_code(P), top,
                               radius, _ptr(t), _ptr(g), _ptr(nn), _ptr(sc), ctypes.byref(nf), _stream(stream)))
     return [Discord(int(t[q]), int(g[q]), int(nn[q]), float(sc[q])) for q in range(nf.value)]
+
+
+def discord_dims(T, rows, t_star: int, m: int, excl: int = -1, n: int | None = None, stream=None):
+    """Alg. 3 Dimension-Detection (self-join mode): (scores, nn, j_star) for the streams `rows`
+    of T (d x ld tensor / array), j_star indexing `rows`."""
+    rows_a = np.ascontiguousarray(rows, dtype=np.int64)
+    n = T.shape[1] if n is None else n
+    sc = np.empty(len(rows_a), np.float64)
+    nn = np.empty(len(rows_a), np.int64)
+    js = _I64()
+    ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+    _check(lib().discord_dims(_ptr(T), ld, n, _dtype_code(T), _ptr(rows_a), len(rows_a), t_star, m, excl,
+                              _ptr(sc), _ptr(nn), ctypes.byref(js), _stream(stream)))
+    return sc, nn, int(js.value)
+

@@ -580,6 +580,7 @@ skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t d
     while (L0 > 256 && tiles(L0) < 2 * 148 * 16) L0 /= 2;
   }
   w.L = (int)round_up(L0, 64);
+  w.span = join_span(dtype);
   w.R = R;
   const int words = dtype == SKMP_F32 ? 1 : 2;
   const size_t qsz = dtype == SKMP_F32 ? 16 : 32;
@@ -793,6 +794,55 @@ skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, 
     score_out[q] = v;
   }
   *n_found = hc;
+  return ok();
+}
+
+skmp_status discord_dims(const void* T, int64_t ld, int64_t n, int32_t dtype, const int64_t* rows,
+                         int64_t nrows, int64_t t_star, int32_t m, int32_t excl, double* scores,
+                         int64_t* nn, int64_t* j_star, void* stream) {
+  if (!T || !rows || !scores || !j_star) return set_error(SKMP_E_INVALID_ARG, "discord_dims: NULL argument");
+  if (dtype != SKMP_F32 && dtype != SKMP_F64) return set_error(SKMP_E_INVALID_ARG, "discord_dims: bad dtype");
+  if (nrows < 1 || m < 2 || ld < n) return set_error(SKMP_E_INVALID_ARG, "discord_dims: need nrows >= 1, m >= 2, ld >= n");
+  if (n < m) return set_error(SKMP_E_SERIES_TOO_SHORT, "discord_dims: n < m");
+  const int64_t n_sub = n - m + 1;
+  if (t_star < 0 || t_star >= n_sub) return set_error(SKMP_E_INVALID_ARG, "discord_dims: t_star outside [0, n-m+1)", t_star);
+  const int ex = excl < 0 ? (m + 1) / 2 : excl;
+  if (t_star - ex - 1 < 0 && t_star + ex + 1 >= n_sub)
+    return set_error(SKMP_E_NO_ADMISSIBLE, "discord_dims: no window farther than excl from t_star");
+  int64_t maxrow = 0;
+  for (int64_t q = 0; q < nrows; ++q) {
+    if (rows[q] < 0) return set_error(SKMP_E_INVALID_ARG, "discord_dims: negative stream row", q);
+    maxrow = std::max(maxrow, rows[q]);
+  }
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  const void* Tdev;
+  int64_t ldd;
+  if ((s = stage_input(T, maxrow + 1, n, ld, dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
+  std::vector<int64_t> hrows(rows, rows + nrows);
+  int64_t* d_rows;
+  if ((s = upload(hrows, &d_rows, tmp)) != SKMP_OK) return s;
+  double* d_score;
+  int64_t* d_nn;
+  char* ws;
+  SKMP_CUDA(tmp.alloc(&d_score, (size_t)nrows));
+  SKMP_CUDA(tmp.alloc(&d_nn, (size_t)nrows));
+  SKMP_CUDA(tmp.alloc(&ws, dims_ws_bytes(nrows, n, m)));
+  SKMP_CUDA(launch_dims(Tdev, ldd, n, dtype, d_rows, nrows, t_star, m, ex, d_score, d_nn, ws, st));
+  std::vector<double> hs((size_t)nrows);
+  std::vector<int64_t> hn((size_t)nrows);
+  SKMP_CUDA(cudaMemcpyAsync(hs.data(), d_score, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaMemcpyAsync(hn.data(), d_nn, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaStreamSynchronize(st));
+  // Alg. 3 lines 3-7: strict '>' over the group in order (reading 20: from -inf)
+  int64_t best = -1;
+  for (int64_t q = 0; q < nrows; ++q)
+    if (best < 0 || hs[(size_t)q] > hs[(size_t)best]) best = q;
+  memcpy(scores, hs.data(), sizeof(double) * nrows);
+  if (nn) memcpy(nn, hn.data(), sizeof(int64_t) * nrows);
+  *j_star = best;
   return ok();
 }
 

@@ -49,6 +49,15 @@ inline int join_width(int dtype) {
   if (dtype == SKMP_F32 && join_x2_enabled()) return join_x2_width();
   return kJoinNT * (dtype == SKMP_F64 ? kJoinD64 : join_d32());
 }
+// candidate-set span of a published profile key: the join publishes the smallest index of a
+// thread's D-cell set, mp_final.cu resolves the set (FP32 scalar: D; x2: its per-group slots)
+int join_x2_span();
+inline int join_span(int dtype) {
+  if (dtype == SKMP_F32 && join_x2_enabled()) return join_x2_span();
+  return dtype == SKMP_F64 ? kJoinD64 : join_d32();
+}
+// FP32 profile keys store (candidate-set base + kKeyArgBias) so that bases down to -(D-1) fit
+constexpr int64_t kKeyArgBias = 32;
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
 inline int64_t join_pad(int dtype) { return join_width(dtype) + 4 * kJoinC + 64; }
 
@@ -92,6 +101,7 @@ struct MpDev {
   int k;
   int64_t n, ld, n_sub, ldq;  // ldq: stride (windows) of the prepared arrays per series
   int m, excl, L;             // L = reseed rows (tile height)
+  int span;                   // candidate-set span of a key (join_span)
   const void* R;              // k x ld (dtype)
   void* Q;                    // k x ldq x {df, dg, inv, 0} (dtype)
   double* mu;                 // k x ldq
@@ -124,6 +134,12 @@ cudaError_t launch_topk(double* C, const int32_t* G, const int64_t* I, int64_t l
                         int top, int radius, int64_t* d_res, int32_t* d_count, void* ws,
                         size_t ws_bytes, cudaStream_t st);
 size_t topk_ws_bytes(int64_t n_sub);
+
+// Alg. 3 dimension detection (K9) — dims.cu.  d_rows [dev] nrows; score/nn [dev] nrows.
+size_t dims_ws_bytes(int64_t nrows, int64_t n, int m);
+cudaError_t launch_dims(const void* X, int64_t ld, int64_t n, int dtype, const int64_t* d_rows,
+                        int64_t nrows, int64_t t_star, int m, int excl, double* score, int64_t* nn,
+                        void* ws, cudaStream_t st);
 
 // kernel-launch accounting (skmp_launch_count): every launcher reports its launches
 void count_launches(int64_t n);

@@ -6,6 +6,17 @@
 
 #include "internal.h"
 
+// The rare publish path of the join kernels: out of line by default; SKMP_PUB_INLINE=1 inlines
+// it (no call-ABI register moves in the hot loop, at the price of hoisted address arithmetic).
+#ifndef SKMP_PUB_INLINE
+#define SKMP_PUB_INLINE 0
+#endif
+#if SKMP_PUB_INLINE
+#define SKMP_PUB_ATTR __device__ __forceinline__
+#else
+#define SKMP_PUB_ATTR __device__ __noinline__
+#endif
+
 namespace skmp {
 namespace join {
 
@@ -33,7 +44,6 @@ struct JoinArgs {
   int m;
   int L;
   int64_t dlo, dhi;
-  unsigned eight;         // = 8 (runtime value on purpose, see join_tile)
   const int64_t* prefix;  // nblk + 1 cumulative tile counts
   int64_t nblk;
   int64_t blk0;
@@ -54,39 +64,6 @@ __device__ __forceinline__ int64_t ord64(double f) {
 __device__ __forceinline__ double unord64(int64_t o) {
   return __longlong_as_double(o >= 0 ? o : (o ^ 0x7FFFFFFFFFFFFFFFll));
 }
-
-// (bits & mask) | d as ONE LOP3 (LUT 0xEC = (a & c) | b): the slot code d is the immediate and
-// the mask ~(D-1) lives in one register shared by every slot, so ptxas neither splits the
-// operation into AND + OR nor materialises a register per code.
-template <int d>
-__device__ __forceinline__ unsigned lop_code_d(unsigned bits, unsigned mask) {
-  unsigned out;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(out) : "r"(bits), "n"(d), "r"(mask));
-  return out;
-}
-template <int d>
-__device__ __forceinline__ float code(float r, unsigned mask) {
-  return __uint_as_float(lop_code_d<d>(__float_as_uint(r), mask));
-}
-template <int d>
-__device__ __forceinline__ double code(double r, unsigned mask) {
-  const int lo = __double2loint(r), hi = __double2hiint(r);
-  return __hiloint2double(hi, (int)lop_code_d<d>((unsigned)lo, mask));
-}
-template <typename T, int d0, int n> struct Coder {
-  // k[d] = code<d>(rho[d]) for d in [d0, d0+n), d a compile-time immediate
-  __device__ static __forceinline__ void run(T* k, const T* rho, unsigned mask) {
-    k[d0] = code<d0>(rho[d0], mask);
-    Coder<T, d0 + 1, n - 1>::run(k, rho, mask);
-  }
-};
-template <typename T, int d0> struct Coder<T, d0, 0> {
-  __device__ static __forceinline__ void run(T*, const T*, unsigned) {}
-};
-template <int D>
-__device__ __forceinline__ int slot_of(float r) { return __float_as_int(r) & (D - 1); }
-template <int D>
-__device__ __forceinline__ int slot_of(double r) { return __double2loint(r) & (D - 1); }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
   float r;
@@ -149,10 +126,11 @@ __device__ __forceinline__ double load_thr(const int64_t* keys, int64_t i, doubl
   return unord64(k);
 }
 
-// publish candidate (v, arg) into profile entry i
+// publish candidate (v, arg) into profile entry i.  arg = smallest index of the candidate set,
+// >= -(D-1) (a column's set may start before row 0); FP32 keys store arg + kKeyArgBias.
 __device__ __forceinline__ void publish(int64_t* keys, int64_t i, float v, int64_t arg) {
   const int64_t key = (int64_t)(((uint64_t)(uint32_t)ord32(v) << 32) |
-                                (uint64_t)(0xFFFFFFFFu - (uint32_t)arg));
+                                (uint64_t)(0xFFFFFFFFu - (uint32_t)(arg + kKeyArgBias)));
   atomicMax(reinterpret_cast<long long*>(keys + i), (long long)key);
 }
 __device__ __forceinline__ void publish(int64_t* keys, int64_t i, double v, int64_t arg) {

@@ -13,14 +13,16 @@
 //    diagonals [delta0 + tD, delta0 + tD + D) and walks the rows in registers (D covariances,
 //    D column operands rotating through registers, D running column maxima).  The recurrence is
 //    2 FFMA + 2 FMUL per cell on the FP32 pipe (or the FP64 pipe for the double variant).
-//  * Index tracking costs one LOP3 per cell: the diagonal slot d = delta mod D is written into
-//    the low log2(D) mantissa bits of rho, so plain (3-input, sm_100 FMNMX3) max operations carry
-//    the argument along; the neighbour's distance is recomputed exactly in FP64 afterwards
-//    (mp_final.cu), so the code bits only ever break near-ties (documented ties).
+//  * Index tracking costs NOTHING per cell: row and column maxima are plain FMNMX(3) trees over
+//    rho values, and a published candidate carries the smallest index of its D-cell set (a row's
+//    D cells in one thread, or a column's D cells in one thread).  mp_final.cu resolves the set
+//    exactly: it evaluates the (<= D) admissible neighbours of the winning set in FP64 and keeps
+//    the nearest (smallest index on ties), so the FP32 recurrence only decides which thread's
+//    set wins (near-ties across sets are documented ties).
 //  * Row maxima reduce over a thread's D slots; column maxima reduce over the D rows a column
 //    spends in a thread.  Each row / column candidate is compared with a shared-memory copy of
 //    the global best ("check then atomic"): only improvements reach the global 64-bit atomicMax
-//    (FP32: packed {orderable rho, ~j}) or 128-bit CAS (FP64).
+//    (FP32: packed {orderable rho, ~base}) or 128-bit CAS (FP64).
 //  * Operands {df, dg, inv} of the tile's rows and columns are staged with cp.async into
 //    shared memory: a ring of W + 2C columns in a swizzled [D][RS/D] layout (conflict-free
 //    128-bit loads: lane t reads column base + tD) and a double-buffered chunk of rows.
@@ -40,26 +42,27 @@ using namespace join;
 
 
 // Rare path: a row / column candidate beat its shared-memory threshold.  Out of line so that
-// none of its address arithmetic is hoisted into the hot loop.
+// none of its address arithmetic is hoisted into the hot loop.  The published argument is the
+// smallest index of the candidate's D-cell set (see mp_final.cu): row i's cells in this thread
+// are j in [i + dt, i + dt + D), column c's cells are i in [c - dt - D + 1, c - dt].
 template <typename T, int D>
-__device__ __noinline__ void publish_pair(int64_t* keys, T* rthr, T* cthr, int rb_u, int ct0, int ct1,
-                                          int64_t i_u, int64_t dt, T rowa, T rowb, T colv0, T colv1) {
-  if (rowa > rthr[rb_u]) {
-    publish(keys, i_u, rowa, i_u + dt + slot_of<D>(rowa));
-    rthr[rb_u] = rowa;
+SKMP_PUB_ATTR void publish_pair(int64_t* keys, typename JT<T>::Q* rowq, T* cthr, int rb_u,
+                                          int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
+                                          T colv0, T colv1) {
+  if (rowa > rowq[rb_u].w) {
+    publish(keys, i_u, rowa, i_u + dt);
+    rowq[rb_u].w = rowa;
   }
-  if (rowb > rthr[rb_u + 1]) {
-    publish(keys, i_u + 1, rowb, i_u + 1 + dt + slot_of<D>(rowb));
-    rthr[rb_u + 1] = rowb;
+  if (rowb > rowq[rb_u + 1].w) {
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt);
+    rowq[rb_u + 1].w = rowb;
   }
   if (colv0 > cthr[ct0]) {
-    const int64_t c = i_u + dt;
-    publish(keys, c, colv0, c - dt - slot_of<D>(colv0));
+    publish(keys, i_u + dt, colv0, i_u - (D - 1));
     cthr[ct0] = colv0;
   }
   if (colv1 > cthr[ct1]) {
-    const int64_t c = i_u + 1 + dt;
-    publish(keys, c, colv1, c - dt - slot_of<D>(colv1));
+    publish(keys, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
     cthr[ct1] = colv1;
   }
 }
@@ -73,8 +76,7 @@ struct Geo {
   static_assert(C % (2 * D) == 0, "chunk must hold whole pairs of D-row rotations");
   static_assert((C & (C - 1)) == 0, "C must be a power of two (row buffer index masking)");
   using Q = typename JT<T>::Q;
-  static constexpr size_t smem_bytes =
-      sizeof(Q) * (RS + 2 * C) + sizeof(T) * (RS + 2 * C);
+  static constexpr size_t smem_bytes = sizeof(Q) * (RS + 2 * C) + sizeof(T) * RS;
   __device__ static __forceinline__ int pos(int64_t c) {
     const int p = (int)(c % RS);
     return (p % D) * RSD + p / D;
@@ -90,57 +92,30 @@ __device__ __forceinline__ void stage_q(typename JT<T>::Q* dst, const typename J
     cp_async16(reinterpret_cast<char*>(dst) + 16 * q, reinterpret_cast<const char*>(src) + 16 * q);
 }
 
-// FP32 key of one cell (no ALU work): y = rho + 2 in [1, 4) computed by the FFMA that also
-// applies inv_i, then the slot code is appended below y's bits by ONE integer multiply-add
-// (FMA pipe): key = (bits(y) - bits(1.0)) * 8 + d, a positive float bit pattern whose order is
-// y's order.  The D slots of a row / column therefore reduce with plain FMNMX(3).
-template <int d>
-__device__ __forceinline__ float key32(float u, float inv_i, unsigned eight) {
-  const float y = fmaf(u, inv_i, 2.0f);
-  unsigned k;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(eight), "n"(0x04000000 + d));
-  return __uint_as_float(k);
-}
-template <typename T, int d0, int n> struct Keyer {
-  // k[d] = key of slot d for d in [d0, d0+n) (compile-time d)
-  __device__ static __forceinline__ void run(T* k, const T* u, T inv_i, unsigned aux) {
-    if constexpr (sizeof(T) == 4) {
-      k[d0] = key32<d0>(u[d0], inv_i, aux);
-    } else {
-      k[d0] = code<d0>(u[d0] * inv_i, aux);  // FP64: rho with the slot in its low mantissa bits
-    }
-    Keyer<T, d0 + 1, n - 1>::run(k, u, inv_i, aux);
-  }
-};
-template <typename T, int d0> struct Keyer<T, d0, 0> {
-  __device__ static __forceinline__ void run(T*, const T*, T, unsigned) {}
-};
-
 // One rotation: D consecutive rows ib .. ib+D-1 (processed as D/2 row pairs) of this thread's D
 // diagonals.  X[(u + d) % D] holds the operands of column ib + u + dt + d at row ib + u.
 template <typename T, int D, int RSD, bool MASKED>
 __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D], T (&CK)[D],
                                          const typename JT<T>::Q* rowp,
                                          const typename JT<T>::Q* ring0,
-                                         const typename JT<T>::Q* ring1, const T* rthp,
-                                         const T* cth0, T* rthr, T* cthr, int rb, int qt,
+                                         const typename JT<T>::Q* ring1,
+                                         const T* cth0, typename JT<T>::Q* rowq, T* cthr, int rb, int qt,
                                          int64_t ib, int64_t dt, const int (&lim)[D],
-                                         int64_t* keys, unsigned aux) {
+                                         int64_t* keys) {
   using Q = typename JT<T>::Q;
 #pragma unroll
   for (int u = 0; u < D; u += 2) {
     // -- row u --
     const Q ra = rowp[u];
     X[(u + D - 1) % D] = (u == 0) ? ring0[((u + D - 1) % D) * RSD] : ring1[((u + D - 1) % D) * RSD];
-    T ka[D], uu[D];
+    T ka[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const Q& x = X[(u + d) % D];
       cov[d] = fma(ra.x, x.y, cov[d]);
       cov[d] = fma(x.x, ra.y, cov[d]);
-      uu[d] = cov[d] * x.z;
+      ka[d] = (cov[d] * x.z) * ra.z;  // rho(i, j) = cov inv_j inv_i
     }
-    Keyer<T, 0, D>::run(ka, uu, ra.z, aux);
     if (MASKED) {
 #pragma unroll
       for (int d = 0; d < D; ++d) ka[d] = ((int)ib + u < lim[d]) ? ka[d] : neg_inf<T>();
@@ -155,9 +130,8 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
       const Q& x = X[(u + 1 + d) % D];
       cov[d] = fma(rbq.x, x.y, cov[d]);
       cov[d] = fma(x.x, rbq.y, cov[d]);
-      uu[d] = cov[d] * x.z;
+      kb[d] = (cov[d] * x.z) * rbq.z;
     }
-    Keyer<T, 0, D>::run(kb, uu, rbq.z, aux);
     if (MASKED) {
 #pragma unroll
       for (int d = 0; d < D; ++d) kb[d] = ((int)ib + u + 1 < lim[d]) ? kb[d] : neg_inf<T>();
@@ -172,10 +146,11 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     const T rowa = tree_max<T, D>(ka);
     const T rowb = tree_max<T, D>(kb);
     // -- check-then-publish (rare) --
-    const bool hit = (rowa > rthp[u]) | (rowb > rthp[u + 1]) | (colv0 > cth0[(u % D) * RSD]) |
+    // row thresholds ride in the row records' 4th word (ra.w, rbq.w): no extra loads
+    const bool hit = (rowa > ra.w) | (rowb > rbq.w) | (colv0 > cth0[(u % D) * RSD]) |
                      (colv1 > cth0[((u + 1) % D) * RSD]);
     if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
-      publish_pair<T, D>(keys, rthr, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+      publish_pair<T, D>(keys, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
                          ib + u, dt, rowa, rowb, colv0, colv1);
     }
   }
@@ -192,7 +167,6 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   Q* ring = reinterpret_cast<Q*>(smem_raw);
   Q* rowq = ring + RS;
   T* cthr = reinterpret_cast<T*>(rowq + 2 * C);
-  T* rthr = cthr + RS;
 
   const int tid = threadIdx.x;
   const int64_t n_sub = a.n_sub;
@@ -256,9 +230,13 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
     stage_q<T>(&rowq[i % (2 * C)], &q[i]);
-    rthr[i % (2 * C)] = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
   }
   cp_async_wait_all();
+  // row thresholds go into the staged row records' 4th word once the copies have landed
+  for (int e = tid; e < C; e += NT) {
+    const int64_t i = i0 + e;
+    rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
+  }
   __syncthreads();  // (one warp per CTA: a warp barrier; kept generic for NT > 32)
 
   // column operand registers: X[(u + d) % D] holds column i + dt + d at unrolled row u
@@ -268,11 +246,6 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   T CK[D];  // running column maxima, same rotation as X
 #pragma unroll
   for (int d = 0; d < D; ++d) CK[d] = neg_inf<T>();
-
-  // one register operand shared by all slot codes (opaque so ptxas keeps it a register):
-  // FP32: the multiplier 8 of the key IMAD; FP64: the LOP3 mask ~(D-1)
-  // (loaded from the kernel parameters so ptxas cannot strength-reduce the IMAD into an ALU LEA)
-  const unsigned aux = (sizeof(T) == 4) ? a.eight : (unsigned)~(D - 1);
 
   // ring row index of column (ib + dt): qt; (ib + dt) is a multiple of D
   int qt = (int)(((i0 + dt) % RS) / D);
@@ -308,24 +281,24 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, rthr + rb, cthr + qt,
-                                  rthr, cthr, rb, qt, ib, dt, lim, keys, aux);
+        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+                                  rowq, cthr, rb, qt, ib, dt, lim, keys);
       else
-        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, rthr + rb, cthr + qt,
-                                   rthr, cthr, rb, qt, ib, dt, lim, keys, aux);
+        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+                                   rowq, cthr, rb, qt, ib, dt, lim, keys);
       qt = qt1;
       rb = (rb + D) & (2 * C - 1);
     }
 
-    // ---- land the prefetched chunk ------------------------------------------------------------
+    // ---- land the prefetched chunk (row thresholds after the row copies landed) --------------
+    cp_async_wait_all();
     if (more) {
 #pragma unroll
       for (int e = 0; e < CPT; ++e) {
         cthr[G::pos(r + delta0 + W + C + tid + e * NT)] = nthr_c[e];
-        rthr[(r + C + tid + e * NT) % (2 * C)] = nthr_r[e];
+        rowq[(r + C + tid + e * NT) % (2 * C)].w = nthr_r[e];
       }
     }
-    cp_async_wait_all();
     __syncthreads();
   }
 
@@ -336,7 +309,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int x = 0; x < D - 1; ++x) {
     const T v = CK[x];
     const int64_t c = i1 + dt + x;
-    if (c < n_sub && v > cthr[G::pos(c)]) publish(keys, c, v, c - dt - slot_of<D>(v));
+    if (c < n_sub && v > cthr[G::pos(c)]) publish(keys, c, v, c - dt - (D - 1));
   }
 }
 
@@ -397,7 +370,6 @@ cudaError_t launch_join_t(const MpDev& w, int64_t dlo, int64_t dhi, const int64_
   a.dlo = dlo;
   a.dhi = dhi;
   a.prefix = prefix;
-  a.eight = 8;
   a.nblk = nblk;
   a.blk0 = blk0;
   const size_t smem = G::smem_bytes;

@@ -10,9 +10,9 @@
 //  * the tile's columns are staged as PAIR records {df_c, df_c+H | dg_c, dg_c+H | inv_c, inv_c+H}
 //    and rows as duplicated records {df_i, df_i | dg_i, dg_i | inv_i, inv_i} so every operand is a
 //    ready-made f32x2 register pair (no per-cell moves);
-//  * per cell: 2 FFMA2 halves (cov) + FMUL2/FFMA2 halves (rho + 2) = 2 packed instructions per
-//    cell, then one IMAD appends the 3-bit slot code (d + DG g) below the key (FMA pipe, no ALU),
-//    and FMNMX3 trees give row and column maxima exactly as in mp_join.cu;
+//  * per cell: 2 FFMA2 halves (cov) + 2 FMUL2 halves (rho) = 2 packed instructions per cell, then
+//    FMNMX3 trees give row and column maxima exactly as in mp_join.cu (no per-cell index work:
+//    a published candidate names its DG-cell set, resolved exactly in mp_final.cu);
 //  * rows/columns publish through the same check-then-atomic path (join_common.cuh).
 // Bit-exact invariance to band splits holds as in mp_join.cu (global re-seed grid, W-aligned
 // diagonal blocks, per-cell arithmetic independent of the band).
@@ -32,8 +32,6 @@ constexpr int NT = 32;            // one warp per CTA
 #define SKMP_X2_DG 8
 #endif
 constexpr int DG = SKMP_X2_DG;    // diagonals per group per thread (2 DG cells per row)
-constexpr unsigned KMUL = 2 * DG; // key multiplier: room for the 2*DG slot codes
-constexpr unsigned KADD = 0u - 0x3F800000u * KMUL;  // (bits(y) - bits(1.0)) * KMUL, mod 2^32
 constexpr int H = NT * DG;        // 128: group B offset; tile width W = 2H
 constexpr int W = 2 * H;
 constexpr int C = kJoinC;         // rows per staged chunk
@@ -69,21 +67,6 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
   return d;
 }
 
-// key of one cell: y = rho + 2 in [1, 4); key = (bits(y) - bits(1.0)) * KMUL + code (IMAD, FMA pipe)
-#ifndef SKMP_X2_LEA_B
-#define SKMP_X2_LEA_B 0  // 1: group-B keys use an ALU shift-add (LEA) instead of the FMA-pipe IMAD
-#endif
-template <int code>
-__device__ __forceinline__ float key_of(float y, unsigned kmul) {
-  unsigned k;
-  if constexpr (SKMP_X2_LEA_B && code >= DG) {
-    k = __float_as_uint(y) * KMUL + (KADD + code);
-  } else {
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(k) : "r"(__float_as_uint(y)), "r"(kmul), "n"(KADD + code));
-  }
-  return __uint_as_float(k);
-}
-
 struct __align__(16) ColRec0 { f2 df, dg; };   // {df_c, df_c+H}, {dg_c, dg_c+H}
 struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 
@@ -95,6 +78,10 @@ struct Smem {
   float thrA[RS];     // column thresholds of group A columns (record base c)
   float thrB[RS];     // ... of group B columns (c + H)
   float rthr[2 * C];
+  // raw next-chunk records / key high words, staged by cp.async (no registers held across the
+  // chunk) and repacked into the pair layout above when the chunk ends
+  float4 rawA[C], rawB[C], rawR[C];
+  int32_t rawtA[C], rawtB[C], rawtR[C];
 };
 
 __device__ __forceinline__ int pos(int64_t c) {
@@ -102,58 +89,48 @@ __device__ __forceinline__ int pos(int64_t c) {
   return (p % DG) * RSD + p / DG;
 }
 
+// masking limits of a thread's diagonals relative to dt (3 registers instead of 2 DG)
+struct Lim {
+  int lo, hi, edge;
+};
+
 // per-slot operand registers
 struct Col {
   f2 df, dg, inv;
 };
 
-template <int DGX, int code0>
-struct Keys {  // k[d] = key(y[d]) with code code0 + d
-  __device__ static __forceinline__ void run(float* k, const float* y, unsigned eight) {
-    k[0] = key_of<code0>(y[0], eight);
-    Keys<DGX - 1, code0 + 1>::run(k + 1, y + 1, eight);
-  }
-};
-template <int code0>
-struct Keys<0, code0> {
-  __device__ static __forceinline__ void run(float*, const float*, unsigned) {}
-};
-
-// Rare path (out of line): publish improved row / column candidates.
-__device__ __noinline__ void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int ctA1,
-                                        int64_t i_u, int64_t dt, float rowa, float rowb,
-                                        float cA0, float cA1, float cB0, float cB1) {
-  auto jrow = [&](float v, int64_t i) {
-    const int s = __float_as_int(v) & (2 * DG - 1);
-    return i + dt + (s & (DG - 1)) + (s >= DG ? H : 0);
-  };
+// Rare path (out of line): publish improved row / column candidates.  The argument is the
+// smallest index of the winning D-cell set (resolved exactly in mp_final.cu): a row's set is one
+// group's DG diagonals of this thread (group B when its maximum is strictly larger: ties go to
+// the smaller indices of group A), a column's set is the DG rows it spent in this thread.
+SKMP_PUB_ATTR void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int ctA1,
+                                        int64_t i_u, int64_t dt, float rowaA, float rowaB,
+                                        float rowbA, float rowbB, float cA0, float cA1, float cB0,
+                                        float cB1) {
+  const float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
   if (rowa > sm->rthr[rbu]) {
-    publish(keys, i_u, rowa, jrow(rowa, i_u));
+    publish(keys, i_u, rowa, i_u + dt + (rowaB > rowaA ? H : 0));
     sm->rthr[rbu] = rowa;
   }
   if (rowb > sm->rthr[rbu + 1]) {
-    publish(keys, i_u + 1, rowb, jrow(rowb, i_u + 1));
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt + (rowbB > rowbA ? H : 0));
     sm->rthr[rbu + 1] = rowb;
   }
-  // group A column c = i + dt (completes after row i): its cells have codes d = c - i' - dt
+  // columns c = i + dt (A) and c + H (B) complete after row i: their rows are [i - DG + 1, i]
   if (cA0 > sm->thrA[ctA0]) {
-    const int64_t c = i_u + dt;
-    publish(keys, c, cA0, c - dt - (__float_as_int(cA0) & (2 * DG - 1)));
+    publish(keys, i_u + dt, cA0, i_u - (DG - 1));
     sm->thrA[ctA0] = cA0;
   }
   if (cA1 > sm->thrA[ctA1]) {
-    const int64_t c = i_u + 1 + dt;
-    publish(keys, c, cA1, c - dt - (__float_as_int(cA1) & (2 * DG - 1)));
+    publish(keys, i_u + 1 + dt, cA1, i_u + 1 - (DG - 1));
     sm->thrA[ctA1] = cA1;
   }
   if (cB0 > sm->thrB[ctA0]) {
-    const int64_t c = i_u + dt + H;
-    publish(keys, c, cB0, c - dt - H - ((__float_as_int(cB0) & (2 * DG - 1)) - DG));
+    publish(keys, i_u + dt + H, cB0, i_u - (DG - 1));
     sm->thrB[ctA0] = cB0;
   }
   if (cB1 > sm->thrB[ctA1]) {
-    const int64_t c = i_u + 1 + dt + H;
-    publish(keys, c, cB1, c - dt - H - ((__float_as_int(cB1) & (2 * DG - 1)) - DG));
+    publish(keys, i_u + 1 + dt + H, cB1, i_u + 1 - (DG - 1));
     sm->thrB[ctA1] = cB1;
   }
 }
@@ -162,26 +139,22 @@ __device__ __noinline__ void publish_x2(int64_t* keys, Smem* sm, int rbu, int ct
 // (u is a loop index of fully unrolled loops, so every register index is a compile-time constant)
 template <bool MASKED>
 __device__ __forceinline__ void row_keys(int u, f2 (&cov)[DG], const Col (&X)[DG], const RowRec0& r0,
-                                         f2 rinv, float (&ka)[DG], float (&kb)[DG], unsigned eight,
-                                         int irow, const int (&limA)[DG], const int (&limB)[DG]) {
-  const f2 two = pk(2.0f, 2.0f);
-  float ya[DG], yb[DG];
+                                         f2 rinv, float (&ka)[DG], float (&kb)[DG],
+                                         int irow, const Lim& lim) {
 #pragma unroll
   for (int d = 0; d < DG; ++d) {
     const Col& x = X[(u + d) % DG];
     cov[d] = fma2(r0.df, x.dg, cov[d]);
     cov[d] = fma2(x.df, r0.dg, cov[d]);
-    const f2 y = fma2(mul2(cov[d], x.inv), rinv, two);
-    ya[d] = lo_of(y);
-    yb[d] = hi_of(y);
+    const f2 rho = mul2(mul2(cov[d], x.inv), rinv);  // rho = cov inv_j inv_i (both groups)
+    ka[d] = lo_of(rho);
+    kb[d] = hi_of(rho);
   }
-  Keys<DG, 0>::run(ka, ya, eight);
-  Keys<DG, DG>::run(kb, yb, eight);
   if (MASKED) {
 #pragma unroll
     for (int d = 0; d < DG; ++d) {
-      ka[d] = (irow < limA[d]) ? ka[d] : neg_inf<float>();
-      kb[d] = (irow < limB[d]) ? kb[d] : neg_inf<float>();
+      ka[d] = (d >= lim.lo && d < lim.hi && irow + d < lim.edge) ? ka[d] : neg_inf<float>();
+      kb[d] = (d >= lim.lo - H && d < lim.hi - H && irow + d < lim.edge - H) ? kb[d] : neg_inf<float>();
     }
   }
 }
@@ -198,22 +171,22 @@ __device__ __forceinline__ void load_col(Col& x, const Smem* sm, int e) {
 template <bool MASKED>
 __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (&CA)[DG], float (&CB)[DG],
                                             Smem* sm, int rb, int qt, int qt1, int64_t ib, int64_t dt,
-                                            const int (&limA)[DG], const int (&limB)[DG],
-                                            int64_t* keys, unsigned eight) {
+                                            const Lim& lim,
+                                            int64_t* keys) {
 #pragma unroll
   for (int u = 0; u < DG; u += 2) {
     // -- row u: its entering column (slot DG-1) takes the register of the column completed at u-1
     load_col(X[(u + DG - 1) % DG], sm, ((u + DG - 1) % DG) * RSD + (u == 0 ? qt : qt1));
     float ka[DG], kb[DG];
-    row_keys<MASKED>(u, cov, X, sm->row0[rb + u], sm->row1[rb + u], ka, kb, eight, (int)ib + u, limA, limB);
+    row_keys<MASKED>(u, cov, X, sm->row0[rb + u], sm->row1[rb + u], ka, kb, (int)ib + u, lim);
     // columns (ib+u)+dt (A) and +H (B) complete after row u
     const float cA0 = max2(CA[u % DG], ka[0]);
     const float cB0 = max2(CB[u % DG], kb[0]);
     // -- row u+1 --
     load_col(X[u % DG], sm, (u % DG) * RSD + qt1);
     float la[DG], lb[DG];
-    row_keys<MASKED>(u + 1, cov, X, sm->row0[rb + u + 1], sm->row1[rb + u + 1], la, lb, eight,
-                     (int)ib + u + 1, limA, limB);
+    row_keys<MASKED>(u + 1, cov, X, sm->row0[rb + u + 1], sm->row1[rb + u + 1], la, lb,
+                     (int)ib + u + 1, lim);
     const float cA1 = max3(CA[(u + 1) % DG], ka[1], la[0]);
     const float cB1 = max3(CB[(u + 1) % DG], kb[1], lb[0]);
 #pragma unroll
@@ -225,23 +198,16 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (
     CB[(u + DG - 1) % DG] = max2(kb[DG - 1], lb[DG - 2]);
     CA[u % DG] = la[DG - 1];
     CB[u % DG] = lb[DG - 1];
-    // -- row maxima over both groups' slots --
-    float ra8[2 * DG], rb8[2 * DG];
-#pragma unroll
-    for (int d = 0; d < DG; ++d) {
-      ra8[d] = ka[d];
-      ra8[DG + d] = kb[d];
-      rb8[d] = la[d];
-      rb8[DG + d] = lb[d];
-    }
-    const float rowa = tree_max<float, 2 * DG>(ra8);
-    const float rowb = tree_max<float, 2 * DG>(rb8);
+    // -- row maxima per group --
+    const float rowaA = tree_max<float, DG>(ka), rowaB = tree_max<float, DG>(kb);
+    const float rowbA = tree_max<float, DG>(la), rowbB = tree_max<float, DG>(lb);
+    const float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
     // -- check-then-publish (rare) --
     const int t0 = (u % DG) * RSD + qt, t1 = ((u + 1) % DG) * RSD + qt;
     const bool hit = (rowa > sm->rthr[rb + u]) | (rowb > sm->rthr[rb + u + 1]) | (cA0 > sm->thrA[t0]) |
                      (cA1 > sm->thrA[t1]) | (cB0 > sm->thrB[t0]) | (cB1 > sm->thrB[t1]);
     if (__any_sync(0xffffffffu, hit))
-      publish_x2(keys, sm, rb + u, t0, t1, ib + u, dt, rowa, rowb, cA0, cA1, cB0, cB1);
+      publish_x2(keys, sm, rb + u, t0, t1, ib + u, dt, rowaA, rowaB, rowbA, rowbB, cA0, cA1, cB0, cB1);
   }
 }
 
@@ -282,6 +248,35 @@ __device__ __forceinline__ void land_row(const RowStage& s, Smem* sm, int64_t i)
   sm->rthr[e] = s.t;
 }
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// next chunk's column record c (and c + H) and row i: raw copies + key high words (the
+// orderable rho of the current best; a possibly stale L1 copy only costs an extra publish)
+__device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int64_t* keys, int64_t c,
+                                           int64_t i, int64_t n_sub, int e) {
+  cp_async16(&sm->rawA[e], q + c);
+  cp_async16(&sm->rawB[e], q + c + H);
+  cp_async16(&sm->rawR[e], q + i);
+  const int32_t inf = 0x7f800000;  // orderable(+inf): never beaten
+  if (c < n_sub) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keys + c) + 4); else sm->rawtA[e] = inf;
+  if (c + H < n_sub) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keys + c + H) + 4); else sm->rawtB[e] = inf;
+  if (i < n_sub) cp_async4(&sm->rawtR[e], reinterpret_cast<const char*>(keys + i) + 4); else sm->rawtR[e] = inf;
+}
+__device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e) {
+  ColStage cs;
+  cs.qa = sm->rawA[e];
+  cs.qb = sm->rawB[e];
+  cs.ta = unord32(sm->rawtA[e]);
+  cs.tb = unord32(sm->rawtB[e]);
+  land_col(cs, sm, c);
+  RowStage rs;
+  rs.q = sm->rawR[e];
+  rs.t = unord32(sm->rawtR[e]);
+  land_row(rs, sm, i);
+}
+
 #ifndef SKMP_X2_MINB
 #define SKMP_X2_MINB 1
 #endif
@@ -300,12 +295,14 @@ join_x2_kernel(JoinArgs a) {
   int64_t* keys = a.keys + (int64_t)g * n_sub;
   const int64_t dt = delta0 + (int64_t)tid * DG;
 
-  int limA[DG], limB[DG];
-#pragma unroll
-  for (int d = 0; d < DG; ++d) {
-    const int64_t da = dt + d, db = dt + d + H;
-    limA[d] = (da >= a.dlo && da < a.dhi && da < n_sub) ? (int)(n_sub - da) : 0;
-    limB[d] = (db >= a.dlo && db < a.dhi && db < n_sub) ? (int)(n_sub - db) : 0;
+  // cell (i, i + dt + d) of group A is valid iff lo <= d < hi and i + d < edge (group B: d + H)
+  Lim lim;
+  {
+    const int64_t big = (int64_t)1 << 30;
+    auto clampi = [&](int64_t v) { return (int)(v < -big ? -big : (v > big ? big : v)); };
+    lim.lo = clampi(a.dlo - dt);
+    lim.hi = clampi(a.dhi - dt);
+    lim.edge = clampi(n_sub - dt);
   }
   const bool diag_masked = (delta0 < a.dlo) || (delta0 + W > a.dhi);
 
@@ -362,18 +359,12 @@ join_x2_kernel(JoinArgs a) {
   float CA[DG], CB[DG];
 #pragma unroll
   for (int d = 0; d < DG; ++d) CA[d] = CB[d] = neg_inf<float>();
-  const unsigned eight = a.eight;  // runtime 8: keeps the key multiply an IMAD (FMA pipe)
   int qt = (int)(((i0 + dt) % RS) / DG);
 
   for (int64_t r = i0; r < i1; r += C) {
     const int64_t rend = (r + C < i1) ? r + C : i1;
     const bool more = r + C < i1;
-    ColStage cs;
-    RowStage rs;
-    if (more) {  // next chunk: record r+delta0+H+C+tid, row r+C+tid
-      fetch_col(cs, q, keys, r + delta0 + H + C + tid, n_sub);
-      fetch_row(rs, q, keys, r + C + tid, n_sub);
-    }
+    if (more) stage_next(&sm, q, keys, r + delta0 + H + C + tid, r + C + tid, n_sub, tid);
     const int nrot = (int)((rend - r) / DG);
     int rb = (int)(r & (2 * C - 1));
     int64_t ib = r;
@@ -381,15 +372,15 @@ join_x2_kernel(JoinArgs a) {
     for (int it = 0; it < nrot; ++it, ib += DG) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, limA, limB, keys, eight);
+        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys);
       else
-        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, limA, limB, keys, eight);
+        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys);
       qt = qt1;
       rb = (rb + DG) & (2 * C - 1);
     }
     if (more) {
-      land_col(cs, &sm, r + delta0 + H + C + tid);
-      land_row(rs, &sm, r + C + tid);
+      cp_async_wait_all();
+      land_next(&sm, r + delta0 + H + C + tid, r + C + tid, tid);
     }
     __syncwarp();
   }
@@ -399,15 +390,15 @@ join_x2_kernel(JoinArgs a) {
   for (int x = 0; x < DG - 1; ++x) {
     const int64_t c = i1 + dt + x;
     const int e = pos(c);
-    if (c < n_sub && CA[x] > sm.thrA[e]) publish(keys, c, CA[x], c - dt - (__float_as_int(CA[x]) & (2 * DG - 1)));
-    if (c + H < n_sub && CB[x] > sm.thrB[e])
-      publish(keys, c + H, CB[x], c - dt - ((__float_as_int(CB[x]) & (2 * DG - 1)) - DG));
+    if (c < n_sub && CA[x] > sm.thrA[e]) publish(keys, c, CA[x], c - dt - (DG - 1));
+    if (c + H < n_sub && CB[x] > sm.thrB[e]) publish(keys, c + H, CB[x], c - dt - (DG - 1));
   }
 }
 
 }  // namespace
 
 int join_x2_width() { return W; }
+int join_x2_span() { return DG; }
 
 bool join_x2_enabled() {
   static const bool on = [] {
@@ -435,7 +426,6 @@ cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const in
   a.prefix = prefix;
   a.nblk = nblk;
   a.blk0 = blk0;
-  a.eight = KMUL;
   dim3 grid((unsigned)ntiles, (unsigned)w.k);
   join_x2_kernel<<<grid, NT, 0, st>>>(a);
   count_launches(1);

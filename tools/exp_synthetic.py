@@ -1,0 +1,131 @@
+#!/usr/bin/env python
+"""The paper's §4.1 synthetic experiment (Fig. 3) on one B200, through the C-ABI.
+
+    python tools/exp_synthetic.py [--d 250,500,1000,2500,5000,7500,10000] [--trials 100]
+                                  [--n 10000] [--m 100] [--dtype f32|f64] [--no-refine]
+
+Per trial: d seeded random-walk streams of n samples, k = ceil(sqrt(d)).
+  exact    : the exact multidimensional discord (Def. 5): the d per-stream self-join
+             profiles (mp_selfjoin on T) -> the ranked list of all (dimension, time) scores;
+  sketched : sketch_build (Alg. 1) + mp_selfjoin on the k sketch series + discord_topk (Alg. 2)
+             + discord_dims over J_{g*} (Alg. 3), optionally + the refinement join of j*
+             (P:L303-304).
+Success: the identified discord (t*, j*)'s exact score ranks within the top 0.01 %
+of the d x n_sub list (rank <= max(1, 1e-4 d n_sub)).  Speedup = exact time / sketched time,
+both on the GPU with CUDA events, the sketched time including sketching.  The
+paper quotes ~50x at d = 10,000 with an almost perfect success rate on
+unstated hardware.  Prints one JSON line per d.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2311_03393_b200 as skmp  # noqa: E402
+
+
+def random_walks(d: int, n: int, seed: int, dtype) -> torch.Tensor:
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    return torch.cumsum(torch.randn((d, n), generator=g, device="cuda", dtype=torch.float64), 1).to(dtype)
+
+
+def timed(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1)
+
+
+def exact(T, m):
+    P, I, inert = skmp.mp_selfjoin(T, m)
+    top = skmp.discord_topk(P, I, inert, m=m, top=1)[0]   # Def. 5: argmax over (dim, time)
+    return P, top
+
+
+def sketched(T, m, k, seed, refine):
+    d = T.shape[0]
+    sk = skmp.sketch_build(T, np.arange(d), k, seed=seed)
+    P, I, inert = skmp.mp_selfjoin(sk.R, m)
+    top = skmp.discord_topk(P, I, inert, m=m, top=1)[0]
+    rows = skmp.group_rows(sk, top.g)
+    _, _, js = skmp.discord_dims(T, rows, top.t, m)
+    j = int(rows[js])
+    t_ref = None
+    if refine:
+        Pj, _, _ = skmp.mp_selfjoin(T[j:j + 1], m)
+        t_ref = int(torch.argmax(Pj[0]))
+    sk.free()
+    return top.t, top.g, j, t_ref
+
+
+def run_d(d, args):
+    m, n = args.m, args.n
+    k = math.ceil(math.sqrt(d))
+    dt = torch.float32 if args.dtype == "f32" else torch.float64
+    n_sub = n - m + 1
+    cut = max(1, int(1e-4 * d * n_sub))
+    ok = ok_ref = 0
+    t_ex, t_sk = [], []
+    ranks = []
+    warm = random_walks(d, n, 1, dt)
+    exact(warm, m)
+    sketched(warm, m, k, 1, not args.no_refine)
+    del warm
+    for trial in range(args.trials):
+        T = random_walks(d, n, 2311033930 + 1000 * d + trial, dt)
+        (P, top_ex), te = timed(lambda: exact(T, m))
+        (t, g, j, t_ref), ts = timed(lambda: sketched(T, m, k, 2311033930 + trial, not args.no_refine))
+        t_ex.append(te)
+        t_sk.append(ts)
+        score = P[j, t]
+        rank = 1 + int((P > score).sum())
+        ranks.append(rank)
+        ok += rank <= cut
+        if t_ref is not None:
+            ok_ref += (1 + int((P > P[j, t_ref]).sum())) <= cut
+        del T, P
+    rec = {
+        "experiment": "paper §4.1 synthetic random walks (P:L364-402)",
+        "d": d, "k": k, "n": n, "m": m, "dtype": args.dtype, "trials": args.trials,
+        "top_fraction": 1e-4, "rank_cut": cut,
+        "success_rate": ok / args.trials,
+        "success_rate_refined": None if args.no_refine else ok_ref / args.trials,
+        "median_rank": statistics.median(ranks),
+        "exact_ms_median": statistics.median(t_ex), "sketched_ms_median": statistics.median(t_sk),
+        "speedup": statistics.median(t_ex) / statistics.median(t_sk),
+        "note": "GPU exact (d self-joins) vs GPU sketched pipeline incl. sketching and Alg. 3"
+                + ("" if args.no_refine else " and the refinement join"),
+    }
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--d", default="250,500,1000,2500,5000,7500,10000")
+    ap.add_argument("--trials", type=int, default=100)
+    ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--m", type=int, default=100)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--no-refine", action="store_true")
+    args = ap.parse_args()
+    assert torch.cuda.is_available(), "the experiment runs on the GPU"
+    for d in [int(x) for x in args.d.split(",")]:
+        run_d(d, args)
+
+
+if __name__ == "__main__":
+    main()
