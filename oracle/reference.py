@@ -18,6 +18,8 @@ Function pins (tests/test_oracle_pins.py):
   detect (identity plan)     -> per-stream exact profiles of Def. 5
   dimension_detection        -> scipy cdist distance profile; exact repeat (periodic stream)
                                 -> score 0; planted single-stream burst -> j* on it
+  abjoin_brute               -> scipy cdist between the two window sets (rows and columns);
+                                a window copied into the other series -> 0 at its copy
 """
 from __future__ import annotations
 
@@ -283,3 +285,31 @@ def refine(r: np.ndarray, m: int, excl: int | None = None):
     P, I, _ = selfjoin_rows(r, m, excl)
     t = int(np.argmax(P))
     return t, int(I[t]), float(P[t]), P, I
+
+
+# ------------------------------------------------------------------------------------------
+# f1: AB-join matrix profile (Def. 6 ab-join) as Alg. 2 uses it:
+# the test series' windows against the training series' windows
+# ------------------------------------------------------------------------------------------
+
+def abjoin_brute(a: np.ndarray, b: np.ndarray, m: int, rows=None):
+    """P[i] = min_j ||z(A_i) - z(B_j)||_2 over ALL windows j of B (no exclusion zone: the two
+    series are different, Def. 6), I[i] = the smallest argmin (reading 8); flat windows per
+    reading 5, each series' flat threshold relative to its own max|x|.  Returns (P, I)."""
+    Za, fa = znorm_windows(a, m)
+    Zb, fb = znorm_windows(b, m)
+    rows = np.arange(Za.shape[0]) if rows is None else np.asarray(rows)
+    P = np.empty(len(rows))
+    I = np.empty(len(rows), dtype=np.int64)
+    B = max(1, 4_000_000 // max(1, Zb.shape[0] * m))
+    for s in range(0, len(rows), B):
+        blk = rows[s:s + B]
+        diff = Za[blk][:, None, :] - Zb[None, :, :]
+        d2 = (diff * diff).sum(axis=2)
+        fi = fa[blk][:, None]
+        fj = fb[None, :]
+        d2 = np.where(fi & fj, 0.0, np.where(fi ^ fj, float(m), d2))
+        idx = np.argmin(d2, axis=1)                 # first occurrence = smallest j
+        P[s:s + len(blk)] = np.sqrt(d2[np.arange(len(blk)), idx])
+        I[s:s + len(blk)] = idx
+    return P, I

@@ -318,3 +318,28 @@ def test_refine_is_top1_of_the_stream_profile():
     t, nn, score, P, I = ref.refine(r, m, excl)
     Pc, Ic = _cdist_profile(r, m, excl)
     assert t == int(np.argmax(Pc)) and abs(score - Pc.max()) < 1e-12 and nn == Ic[t]
+
+
+# ---------------------------------------------------------------------------------- AB-join
+@pytest.mark.parametrize("seed", range(6))
+def test_abjoin_brute_vs_cdist_and_planted(seed):
+    """Def. 6 ab-join: pinned to scipy cdist on the two window sets; both
+    directions (A against B is the transpose of B against A); a window of A copied into B
+    scores 0 at its copy."""
+    rng = np.random.default_rng([seed, 31])
+    m = [8, 16, 32][seed % 3]
+    a = synthgen.mp_series(1, int(rng.integers(3 * m, 260)), seed=seed, kind="mix")[0]
+    b = synthgen.mp_series(1, int(rng.integers(3 * m, 260)), seed=seed + 100, kind="randwalk")[0]
+    t = int(rng.integers(0, len(a) - m + 1))
+    u = int(rng.integers(0, len(b) - m + 1))
+    b[u:u + m] = 2.0 * a[t:t + m] - 1.0                    # affine copy: z-normalised identical
+    P, I = ref.abjoin_brute(a, b, m)
+    Za, _ = ref.znorm_windows(a, m)
+    Zb, _ = ref.znorm_windows(b, m)
+    D = cdist(Za, Zb)                                       # library Euclidean distances
+    np.testing.assert_allclose(P, D.min(axis=1), rtol=1e-12, atol=1e-12)
+    for i in np.where(I != D.argmin(axis=1))[0]:
+        assert abs(D[i, I[i]] - D[i].min()) < 1e-12
+    Pt, It = ref.abjoin_brute(b, a, m)
+    np.testing.assert_allclose(Pt, D.min(axis=0), rtol=1e-12, atol=1e-12)
+    assert P[t] < 1e-6 and Pt[u] < 1e-6
