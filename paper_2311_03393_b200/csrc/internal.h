@@ -37,13 +37,16 @@ constexpr double kFlatEps = 1e-12;  // readings 4/5
 // rounding unit of mp_band; rows per chunk C; a tile spans `reseed_rows` rows.
 constexpr int kJoinNT = 32;   // one warp per CTA: no CTA-wide barriers in the hot loop
 constexpr int kJoinD32 = 8;    // default diagonals per thread (FP32); 16 selectable (SKMP_JOIN_D)
-constexpr int kJoinD64 = 8;
+#ifndef SKMP_JOIN_D64
+#define SKMP_JOIN_D64 4
+#endif
+constexpr int kJoinD64 = SKMP_JOIN_D64;  // diagonals per thread of the FP64 join (4 | 8)
 #ifndef SKMP_JOIN_C
 #define SKMP_JOIN_C 32
 #endif
 constexpr int kJoinC = SKMP_JOIN_C;  // rows per staged chunk (power of two, multiple of 2D)
 int join_d32();                // diagonals per thread of the FP32 join (env SKMP_JOIN_D: 8 | 16)
-bool join_x2_enabled();        // packed f32x2 FP32 join selected (SKMP_JOIN_IMPL=x2)
+bool join_x2_enabled();        // packed f32x2 FP32 join (default; SKMP_JOIN_IMPL=scalar disables)
 int join_x2_width();           // its tile width
 inline int join_width(int dtype) {
   if (dtype == SKMP_F32 && join_x2_enabled()) return join_x2_width();
@@ -117,7 +120,7 @@ cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
 // band join: tiles described by blocks of W diagonals [dlo, dhi)
 cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
-// packed f32x2 FP32 join (mp_join_x2.cu), opt-in with SKMP_JOIN_IMPL=x2
+// packed f32x2 FP32 join (mp_join_x2.cu), the default FP32 join
 cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
                               int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
 cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);

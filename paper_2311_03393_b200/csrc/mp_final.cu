@@ -22,7 +22,7 @@ __device__ __forceinline__ bool key_arg(const int64_t* keys, int64_t i, int word
   if (words == 1) {
     const uint32_t lo = (uint32_t)(keys[i] & 0xFFFFFFFFll);
     const int32_t hi = (int32_t)(keys[i] >> 32);
-    if (hi == (int32_t)0x807FFFFF && lo == 0) return false;  // never written
+    if (hi == (int32_t)0x80800000 && lo == 0) return false;  // never written (init key)
     *base = (int64_t)(0xFFFFFFFFu - lo) - kKeyArgBias;
     return true;
   }
@@ -203,8 +203,13 @@ __global__ void finalize_kernel(MpDev w, const int32_t* __restrict__ nflat, T* _
 cudaError_t launch_mp_finalize(const MpDev& w, void* P, int64_t* I, cudaStream_t st) {
   const int64_t threads = w.n_sub * 32;
   dim3 grid((unsigned)((threads + 255) / 256), (unsigned)w.k);
-  if (w.span != 8 && w.span != 16) return cudaErrorInvalidValue;
-  if (w.dtype == SKMP_F32) {
+  if (w.span != 4 && w.span != 8 && w.span != 16) return cudaErrorInvalidValue;
+  if (w.span == 4) {
+    if (w.dtype == SKMP_F32)
+      finalize_kernel<float, 4><<<grid, 256, 0, st>>>(w, w.nflat, static_cast<float*>(P), I);
+    else
+      finalize_kernel<double, 4><<<grid, 256, 0, st>>>(w, w.nflat, static_cast<double*>(P), I);
+  } else if (w.dtype == SKMP_F32) {
     if (w.span == 16)
       finalize_kernel<float, 16><<<grid, 256, 0, st>>>(w, w.nflat, static_cast<float*>(P), I);
     else

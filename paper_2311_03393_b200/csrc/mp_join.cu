@@ -49,19 +49,19 @@ template <typename T, int D>
 SKMP_PUB_ATTR void publish_pair(int64_t* keys, typename JT<T>::Q* rowq, T* cthr, int rb_u,
                                           int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
                                           T colv0, T colv1) {
-  if (rowa > rowq[rb_u].w) {
+  if (rowa >= rowq[rb_u].w) {
     publish(keys, i_u, rowa, i_u + dt);
     rowq[rb_u].w = rowa;
   }
-  if (rowb > rowq[rb_u + 1].w) {
+  if (rowb >= rowq[rb_u + 1].w) {
     publish(keys, i_u + 1, rowb, i_u + 1 + dt);
     rowq[rb_u + 1].w = rowb;
   }
-  if (colv0 > cthr[ct0]) {
+  if (colv0 >= cthr[ct0]) {
     publish(keys, i_u + dt, colv0, i_u - (D - 1));
     cthr[ct0] = colv0;
   }
-  if (colv1 > cthr[ct1]) {
+  if (colv1 >= cthr[ct1]) {
     publish(keys, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
     cthr[ct1] = colv1;
   }
@@ -147,8 +147,10 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     const T rowb = tree_max<T, D>(kb);
     // -- check-then-publish (rare) --
     // row thresholds ride in the row records' 4th word (ra.w, rbq.w): no extra loads
-    const bool hit = (rowa > ra.w) | (rowb > rbq.w) | (colv0 > cth0[(u % D) * RSD]) |
-                     (colv1 > cth0[((u + 1) % D) * RSD]);
+    // ">=": a candidate EQUAL to the current best is published too, so exact ties always reach
+    // the atomic (smallest set wins) and keys do not depend on the tile order / band split
+    const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
+                     (colv1 >= cth0[((u + 1) % D) * RSD]);
     if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
       publish_pair<T, D>(keys, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
                          ib + u, dt, rowa, rowb, colv0, colv1);
@@ -309,7 +311,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int x = 0; x < D - 1; ++x) {
     const T v = CK[x];
     const int64_t c = i1 + dt + x;
-    if (c < n_sub && v > cthr[G::pos(c)]) publish(keys, c, v, c - dt - (D - 1));
+    if (c < n_sub && v >= cthr[G::pos(c)]) publish(keys, c, v, c - dt - (D - 1));
   }
 }
 
@@ -397,7 +399,7 @@ cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64
                            int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
   if (w.dtype == SKMP_F32) {
-    if (join_x2_enabled() && join_d32() == 8)
+    if (join_x2_enabled())
       return launch_mp_join_x2(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
     if (join_d32() == 16) return launch_join_t<float, 16>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
     return launch_join_t<float, 8>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);

@@ -23,6 +23,17 @@
 #include "internal.h"
 #include "join_common.cuh"
 
+// The rare publish path is inlined here (measured: the out-of-line call costs ~0.3 register
+// moves per cell in the hot loop); SKMP_X2_PUB_INLINE=0 restores the call.
+#ifndef SKMP_X2_PUB_INLINE
+#define SKMP_X2_PUB_INLINE 1
+#endif
+#if SKMP_X2_PUB_INLINE
+#define SKMP_X2_PUB_ATTR __device__ __forceinline__
+#else
+#define SKMP_X2_PUB_ATTR __device__ __noinline__
+#endif
+
 namespace skmp {
 namespace {
 using namespace join;
@@ -103,33 +114,33 @@ struct Col {
 // smallest index of the winning D-cell set (resolved exactly in mp_final.cu): a row's set is one
 // group's DG diagonals of this thread (group B when its maximum is strictly larger: ties go to
 // the smaller indices of group A), a column's set is the DG rows it spent in this thread.
-SKMP_PUB_ATTR void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int ctA1,
+SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int ctA1,
                                         int64_t i_u, int64_t dt, float rowaA, float rowaB,
                                         float rowbA, float rowbB, float cA0, float cA1, float cB0,
                                         float cB1) {
   const float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
-  if (rowa > sm->rthr[rbu]) {
+  if (rowa >= sm->rthr[rbu]) {
     publish(keys, i_u, rowa, i_u + dt + (rowaB > rowaA ? H : 0));
     sm->rthr[rbu] = rowa;
   }
-  if (rowb > sm->rthr[rbu + 1]) {
+  if (rowb >= sm->rthr[rbu + 1]) {
     publish(keys, i_u + 1, rowb, i_u + 1 + dt + (rowbB > rowbA ? H : 0));
     sm->rthr[rbu + 1] = rowb;
   }
   // columns c = i + dt (A) and c + H (B) complete after row i: their rows are [i - DG + 1, i]
-  if (cA0 > sm->thrA[ctA0]) {
+  if (cA0 >= sm->thrA[ctA0]) {
     publish(keys, i_u + dt, cA0, i_u - (DG - 1));
     sm->thrA[ctA0] = cA0;
   }
-  if (cA1 > sm->thrA[ctA1]) {
+  if (cA1 >= sm->thrA[ctA1]) {
     publish(keys, i_u + 1 + dt, cA1, i_u + 1 - (DG - 1));
     sm->thrA[ctA1] = cA1;
   }
-  if (cB0 > sm->thrB[ctA0]) {
+  if (cB0 >= sm->thrB[ctA0]) {
     publish(keys, i_u + dt + H, cB0, i_u - (DG - 1));
     sm->thrB[ctA0] = cB0;
   }
-  if (cB1 > sm->thrB[ctA1]) {
+  if (cB1 >= sm->thrB[ctA1]) {
     publish(keys, i_u + 1 + dt + H, cB1, i_u + 1 - (DG - 1));
     sm->thrB[ctA1] = cB1;
   }
@@ -204,8 +215,9 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (
     const float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
     // -- check-then-publish (rare) --
     const int t0 = (u % DG) * RSD + qt, t1 = ((u + 1) % DG) * RSD + qt;
-    const bool hit = (rowa > sm->rthr[rb + u]) | (rowb > sm->rthr[rb + u + 1]) | (cA0 > sm->thrA[t0]) |
-                     (cA1 > sm->thrA[t1]) | (cB0 > sm->thrB[t0]) | (cB1 > sm->thrB[t1]);
+    // ">=": exact ties always reach the atomic (keys independent of tile order / band split)
+    const bool hit = (rowa >= sm->rthr[rb + u]) | (rowb >= sm->rthr[rb + u + 1]) | (cA0 >= sm->thrA[t0]) |
+                     (cA1 >= sm->thrA[t1]) | (cB0 >= sm->thrB[t0]) | (cB1 >= sm->thrB[t1]);
     if (__any_sync(0xffffffffu, hit))
       publish_x2(keys, sm, rb + u, t0, t1, ib + u, dt, rowaA, rowaB, rowbA, rowbB, cA0, cA1, cB0, cB1);
   }
@@ -278,7 +290,7 @@ __device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e)
 }
 
 #ifndef SKMP_X2_MINB
-#define SKMP_X2_MINB 1
+#define SKMP_X2_MINB 16  // <= 128 registers: 16 warps / SM (measured best)
 #endif
 __global__ void __launch_bounds__(NT, SKMP_X2_MINB)
 join_x2_kernel(JoinArgs a) {
@@ -390,8 +402,8 @@ join_x2_kernel(JoinArgs a) {
   for (int x = 0; x < DG - 1; ++x) {
     const int64_t c = i1 + dt + x;
     const int e = pos(c);
-    if (c < n_sub && CA[x] > sm.thrA[e]) publish(keys, c, CA[x], c - dt - (DG - 1));
-    if (c + H < n_sub && CB[x] > sm.thrB[e]) publish(keys, c + H, CB[x], c - dt - (DG - 1));
+    if (c < n_sub && CA[x] >= sm.thrA[e]) publish(keys, c, CA[x], c - dt - (DG - 1));
+    if (c + H < n_sub && CB[x] >= sm.thrB[e]) publish(keys, c + H, CB[x], c - dt - (DG - 1));
   }
 }
 
@@ -403,7 +415,8 @@ int join_x2_span() { return DG; }
 bool join_x2_enabled() {
   static const bool on = [] {
     const char* e = getenv("SKMP_JOIN_IMPL");
-    return e && e[0] == 'x';  // opt-in ("x2"); measured slower than mp_join.cu on B200
+    // default; SKMP_JOIN_IMPL=scalar (or SKMP_JOIN_D=16) selects mp_join.cu's FP32 kernel
+    return !(e && e[0] == 's') && join_d32() == 8;
   }();
   return on;
 }

@@ -101,13 +101,14 @@ prep_kernel(MpDev w) {
 }
 
 __global__ void keys_init_kernel(int64_t* keys, int64_t count, int words) {
-  // FP32 key: (orderable(-inf) << 32) | 0;  FP64 key: {orderable64(-inf), INT64_MIN}
+  // FP32 key: (orderable(-FLT_MAX) << 32) | 0;  FP64 key: {orderable64(-DBL_MAX), INT64_MIN}.
+  // -MAX rather than -inf: masked cells are -inf and must never pass the join's ">=" check.
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   if (words == 1) {
-    keys[i] = (int64_t)(((uint64_t)(uint32_t)0x807FFFFFu) << 32);
+    keys[i] = (int64_t)(((uint64_t)(uint32_t)0x80800000u) << 32);
   } else {
-    keys[2 * i] = (int64_t)0x800FFFFFFFFFFFFFull;
+    keys[2 * i] = (int64_t)0x8010000000000000ull;
     keys[2 * i + 1] = INT64_MIN;
   }
 }
