@@ -10,6 +10,7 @@ FP32, 20 injected discords):
   a5     sketch_add_dim of 500 new streams + sketch_del_dim of 500 originals (§3.3)
   a6-a9  mp_create (window prep) + mp_join (the diagonal recurrence) + mp_finalize
   a10-11 discord_topk (Alg. 2 combine + ordered top-K)
+  f2     discord_dims over the top discord's group (Alg. 3 dimension detection)
 Multi-GPU (torchrun, N>1): streams are sharded over ranks, partial sketches are sum-all-reduced
 (NCCL), each rank joins its diagonal band (mp_band) and the profile keys are max-all-reduced
 (NCCL); rank 0 finalizes and ranks the discords.  Strong scaling (fixed total work).
@@ -61,6 +62,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reseed", type=int, default=0)
     return ap.parse_args()
+
+
+def join_kernel_name(dtype: str) -> str:
+    if dtype == "f32" and os.environ.get("SKMP_JOIN_IMPL", "x2")[:1] != "s" and os.environ.get("SKMP_JOIN_D", "8") == "8":
+        return "join_x2_kernel (mp_join_x2.cu, packed f32x2)"
+    return "join_kernel (mp_join.cu)"
 
 
 def peaks():
@@ -249,7 +256,7 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(T, Ta, Tdl, timers=None):
-        e = [ev() for _ in range(6)] if timers is not None else None
+        e = [ev() for _ in range(7)] if timers is not None else None
         if e: e[0].record()
         sk = skmp.sketch_build(T, my_ids, k, seed=cfg.seed)
         if e: e[1].record()
@@ -272,11 +279,22 @@ def main():
             P, I, inert = skmp.mp_finalize(w)
             res = skmp.discord_topk(P, I, inert, m=m, top=top)
         w.free()
+        if e: e[5].record()
+        # Alg. 3: the dimension j* of the top discord inside its group J_g*
+        tg = torch.tensor([res[0].t, res[0].g] if rank == 0 else [0, 0], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.broadcast(tg, 0)
+        t_star, g_star = (int(x) for x in tg.tolist())
+        sources = [(T, my_ids), (Ta, my_add)]
+        if world > 1:
+            dim = sdist.detect_dimension_dist(sk, sources, t_star, g_star, m, dev)
+        else:
+            dim = skmp.detect_dimension(sk, sources, t_star, g_star, m)
         sk.free()
         if e:
-            e[5].record()
+            e[6].record()
             timers.append(e)
-        return res
+        return res, dim
 
     def barrier():
         if world > 1:
@@ -309,6 +327,7 @@ def main():
         "mp_prep_ms": statistics.mean(e[2].elapsed_time(e[3]) for e in timers),
         "mp_join_ms": statistics.mean(e[3].elapsed_time(e[4]) for e in timers),
         "finalize_topk_ms": statistics.mean(e[4].elapsed_time(e[5]) for e in timers),
+        "alg3_dims_ms": statistics.mean(e[5].elapsed_time(e[6]) for e in timers),
     }
     t = torch.tensor([elapsed_ms, phase["mp_join_ms"]], device=dev, dtype=torch.float64)
     if world > 1:
@@ -346,7 +365,7 @@ def main():
             hb = torch.tensor([h2d], device=dev, dtype=torch.float64)
             dist.all_reduce(hb)
             h2d = int(hb.item())
-        d2h = top * (8 + 4 + 8 + 8) + 4
+        d2h = top * (8 + 4 + 8 + 8) + 4 + 16  # top-K tuples + count + Alg. 3 result
         e2e = {"value": cells_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms}
 
@@ -381,7 +400,7 @@ def main():
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "join_kernel (mp_join.cu)",
+                     "kernel": join_kernel_name(cfg.dtype),
                      "note": f"{FLOPS_PER_CELL} algorithmic FLOP per cell x cells of this rank's band / mean "
                              f"mp_join event time; peak = 148 SM x {128 if cfg.dtype == 'f32' else 64} lanes x 2 x "
                              f"1.965 GHz (derived, DESIGN.md §6)",
@@ -397,7 +416,11 @@ def main():
         "e2e": e2e,
     }
     if res is not None:
+        res, dim = res
         out["top"] = [(d.t, d.g, round(d.score, 4)) for d in res[:8]]
+        if dim is not None:
+            out["alg3"] = {"t": res[0].t, "g": res[0].g, "j_star_id": dim[0], "score": round(dim[1], 4),
+                           "nn": dim[2]}
     if world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         v, nrows, dt = oracle_sample(cfg, 12.0, threads)

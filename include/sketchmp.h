@@ -198,6 +198,26 @@ void mp_free(skmp_mp* w);
 skmp_status mp_selfjoin(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
                         const skmp_mp_cfg* cfg, void* P, int64_t* I, uint8_t* inert, void* stream);
 
+/* AB-join matrix profile (Def. 6 ab-join), the join Alg. 2 calls as written
+ * (ABjoinMP(R_train^(g), R_test^(g), m)):
+ *
+ *   PA_g[i] = min_j dist(A^(g)_{i,m}, B^(g)_{j,m}),  IA_g[i] = smallest argmin,  over ALL windows
+ *   j of B (two different series: no exclusion zone), and optionally the reverse profile PB of B
+ *   against A (it comes from the same cells; pass PB = IB = NULL to skip it).
+ *   RA  [dev] k x ldA test series (nA samples);  RB [dev] k x ldB train series (nB samples).
+ *   cfg m >= 2 (excl is ignored), reseed_rows as for mp_create.
+ *   PA [dev] k x (nA-m+1) dtype, IA [dev] k x (nA-m+1) int64 (indices into B's windows);
+ *   PB/IB likewise k x (nB-m+1) or NULL;  inert [host] k or NULL: 1 where both series of a group
+ *   are entirely flat (an empty group, reading 6).
+ * Flat windows follow reading 5 (each series' threshold relative to its own max|x|).  Computed
+ * as two diagonal-band passes of the same join kernels (test rows against train columns, and
+ * train rows against test columns), each cell once; neighbours resolved exactly in FP64 as in
+ * mp_finalize.  Synchronous (window preparation).  Errors: INVALID_ARG, SERIES_TOO_SHORT, CUDA,
+ * OOM. */
+skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, int64_t nB, int64_t ldB,
+                      int32_t k, int32_t dtype, const skmp_mp_cfg* cfg, void* PA, int64_t* IA, void* PB,
+                      int64_t* IB, uint8_t* inert, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Discord detection over the sketch profiles: Alg. 2 Time-Detection + ordered
  * top-K list (reading 12):

@@ -5,7 +5,7 @@ PyTorch supplies device memory and the current CUDA stream.  The same names as t
 
     sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
     sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
-    mp_selfjoin, discord_topk, discord_dims
+    mp_selfjoin, mp_abjoin, discord_topk, discord_dims
 
 There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
 without a GPU return SKMP_E_CUDA (raised as SkmpError).
@@ -83,6 +83,8 @@ _SIGS = {
     "mp_selfjoin": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
     "discord_topk": (ctypes.c_int, [_P, _P, _P, _I32, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
                                     _P, _P]),
+    "mp_abjoin": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _I64, _I32, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P,
+                                 _P, _P]),
     "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
 }
 
@@ -394,6 +396,27 @@ class Discord:
     score: float
 
 
+def mp_abjoin(RA, RB, m: int, *, reseed_rows: int = 0, both: bool = False, stream=None):
+    """AB-join (Def. 6): profile of the test series RA (k x nA) against the train series RB
+    (k x nB), same dtype, CUDA tensors.  Returns (PA, IA, inert) or, with both=True,
+    (PA, IA, PB, IB, inert)."""
+    import torch
+    k, nA = RA.shape
+    nB = RB.shape[1]
+    assert RB.shape[0] == k and RA.dtype == RB.dtype
+    PA = torch.empty((k, nA - m + 1), dtype=RA.dtype, device=RA.device)
+    IA = torch.empty((k, nA - m + 1), dtype=torch.int64, device=RA.device)
+    PB = torch.empty((k, nB - m + 1), dtype=RA.dtype, device=RA.device) if both else None
+    IB = torch.empty((k, nB - m + 1), dtype=torch.int64, device=RA.device) if both else None
+    inert = np.zeros(k, dtype=np.uint8)
+    cfg = _mpcfg(m, -1, reseed_rows)
+    _check(lib().mp_abjoin(_ptr(RA), nA, RA.stride(0), _ptr(RB), nB, RB.stride(0), k, _dtype_code(RA),
+                           ctypes.byref(cfg), _ptr(PA), _ptr(IA), _ptr(PB), _ptr(IB), _ptr(inert), _stream(stream)))
+    if both:
+        return PA, IA, PB, IB, inert.astype(bool)
+    return PA, IA, inert.astype(bool)
+
+
 def discord_topk(P, I, inert, m: int, top: int, radius: int = -1, stream=None) -> list[Discord]:
     k, n_sub = P.shape
     inert_a = None if inert is None else np.ascontiguousarray(inert, dtype=np.uint8)
@@ -419,4 +442,29 @@ def discord_dims(T, rows, t_star: int, m: int, excl: int = -1, n: int | None = N
     _check(lib().discord_dims(_ptr(T), ld, n, _dtype_code(T), _ptr(rows_a), len(rows_a), t_star, m, excl,
                               _ptr(sc), _ptr(nn), ctypes.byref(js), _stream(stream)))
     return sc, nn, int(js.value)
+
+
+def detect_dimension(sk: Sketch, sources, t: int, g: int, m: int, excl: int = -1, stream=None):
+    """Alg. 3 over J_g for the discord at time t, with the group's streams spread over several
+    device matrices: `sources` = [(T, ids), ...] (rows of T hold the streams with those ids).
+    Returns (id*, score, nn) with Alg. 3's tie rule (first strict maximiser in plan order), or
+    None when no stream of J_g is in `sources`."""
+    pl = sketch_plan(sk)
+    members = pl["ids"] if np.all(pl["groups"] < 0) else pl["ids"][pl["groups"] == g]
+    order = {int(j): q for q, j in enumerate(members)}
+    best = None
+    for T, ids in sources:
+        if T is None or len(ids) == 0:
+            continue
+        ids = np.asarray(ids, dtype=np.uint64)
+        rows = np.array([q for q, j in enumerate(ids) if int(j) in order], dtype=np.int64)
+        if len(rows) == 0:
+            continue
+        sc, nn, _ = discord_dims(T, rows, t, m, excl, stream=stream)
+        for q in range(len(rows)):
+            j = int(ids[rows[q]])
+            cand = (float(sc[q]), -order[j], j, int(nn[q]))
+            if best is None or cand[:2] > best[:2]:
+                best = cand
+    return None if best is None else (best[2], best[0], best[3])
 

@@ -529,7 +529,7 @@ namespace {
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 skmp_status mp_validate(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
-                        const skmp_mp_cfg* cfg, int* excl) {
+                        const skmp_mp_cfg* cfg, int* excl, bool ab = false) {
   if (!R || !cfg) return set_error(SKMP_E_INVALID_ARG, "mp: NULL argument");
   if (k < 1 || n < 1 || ld < n) return set_error(SKMP_E_INVALID_ARG, "mp: need k >= 1, n >= 1, ld >= n");
   if (dtype != SKMP_F32 && dtype != SKMP_F64) return set_error(SKMP_E_INVALID_ARG, "mp: bad dtype");
@@ -539,6 +539,10 @@ skmp_status mp_validate(const void* R, int32_t k, int64_t n, int64_t ld, int32_t
   const int64_t n_sub = n - cfg->m + 1;
   if (n_sub >= (int64_t)INT32_MAX - 1) return set_error(SKMP_E_INVALID_ARG, "mp: n_sub must be < 2^31");
   *excl = cfg->excl < 0 ? (cfg->m + 1) / 2 : cfg->excl;
+  if (ab) {  // AB-join: two different series, no exclusion zone (Def. 6)
+    *excl = -1;
+    return SKMP_OK;
+  }
   if (n_sub < 2 * (int64_t)(*excl) + 2)
     return set_error(SKMP_E_NO_ADMISSIBLE, "mp: n_sub < 2*excl + 2 (some row has no admissible neighbour)");
   return SKMP_OK;
@@ -547,10 +551,13 @@ skmp_status mp_validate(const void* R, int32_t k, int64_t n, int64_t ld, int32_t
 
 extern "C" {
 
-skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
-                      const skmp_mp_cfg* cfg, void* stream, skmp_mp** out) {
+}  // extern "C"
+
+namespace {
+skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                           const skmp_mp_cfg* cfg, void* stream, skmp_mp** out, bool ab) {
   int excl = 0;
-  skmp_status s = mp_validate(R, k, n, ld, dtype, cfg, &excl);
+  skmp_status s = mp_validate(R, k, n, ld, dtype, cfg, &excl, ab);
   if (s) return s;
   if (!out) return set_error(SKMP_E_INVALID_ARG, "mp_create: NULL out");
   if ((s = require_device()) != SKMP_OK) return s;
@@ -633,6 +640,37 @@ skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t d
   return ok();
 }
 
+// tiles of the diagonal band [lo, hi) of rows wr against columns wc, then the join launch
+skmp_status join_band(const MpDev& wr, const MpDev& wc, int64_t lo, int64_t hi, cudaStream_t st) {
+  if (lo >= hi) return SKMP_OK;
+  const int64_t W = join_width(wr.dtype);
+  const int64_t blk0 = lo / W, blk1 = (hi + W - 1) / W;
+  const int64_t nblk = blk1 - blk0;
+  std::vector<int64_t> prefix((size_t)nblk + 1, 0);
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t d0 = (blk0 + b) * W;
+    const int64_t dmin = d0 > lo ? d0 : lo;
+    const int64_t rows = tile_rows(wr.n_sub, wc.n_sub, dmin);
+    prefix[(size_t)b + 1] = prefix[(size_t)b] + (rows > 0 ? (rows + wr.L - 1) / wr.L : 0);
+  }
+  const int64_t ntiles = prefix[(size_t)nblk];
+  if (ntiles > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "mp_join: too many tiles; raise reseed_rows");
+  Temps tmp(st);
+  int64_t* d_prefix = nullptr;
+  skmp_status s = upload(prefix, &d_prefix, tmp);
+  if (s) return s;
+  SKMP_CUDA(launch_mp_join(wr, wc, lo, hi, d_prefix, nblk, ntiles, blk0, st));
+  return SKMP_OK;
+}
+}  // namespace
+
+extern "C" {
+
+skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                      const skmp_mp_cfg* cfg, void* stream, skmp_mp** out) {
+  return mp_create_impl(R, k, n, ld, dtype, cfg, stream, out, false);
+}
+
 skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, int32_t band,
                     int64_t* diag_lo, int64_t* diag_hi) {
   if (nbands < 1 || band < 0 || band >= nbands || !diag_lo || !diag_hi || n_sub < 2 || excl < 0)
@@ -684,23 +722,8 @@ skmp_status mp_join(skmp_mp* h, int64_t diag_lo, int64_t diag_hi, void* stream) 
   if (lo < w.excl + 1) lo = w.excl + 1;
   if (hi > w.n_sub) hi = w.n_sub;
   if (lo >= hi) return ok();
-  const int64_t W = join_width(w.dtype);
-  const int64_t blk0 = lo / W, blk1 = (hi + W - 1) / W;
-  const int64_t nblk = blk1 - blk0;
-  std::vector<int64_t> prefix((size_t)nblk + 1, 0);
-  for (int64_t b = 0; b < nblk; ++b) {
-    const int64_t d0 = (blk0 + b) * W;
-    const int64_t dmin = d0 > lo ? d0 : lo;
-    const int64_t rows = w.n_sub - dmin;
-    prefix[(size_t)b + 1] = prefix[(size_t)b] + (rows + w.L - 1) / w.L;
-  }
-  const int64_t ntiles = prefix[(size_t)nblk];
-  if (ntiles > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "mp_join: too many tiles; raise reseed_rows");
-  Temps tmp(st);
-  int64_t* d_prefix = nullptr;
-  skmp_status s = upload(prefix, &d_prefix, tmp);
+  skmp_status s = join_band(w, w, lo, hi, st);
   if (s) return s;
-  SKMP_CUDA(launch_mp_join(w, lo, hi, d_prefix, nblk, ntiles, blk0, st));
   h->st = st;
   return ok();
 }
@@ -717,7 +740,7 @@ skmp_status mp_keys(skmp_mp* h, void** keys, int64_t* count, int32_t* words) {
 skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* stream) {
   if (!h || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize: NULL argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SKMP_CUDA(launch_mp_finalize(h->w, P, I, st));
+  SKMP_CUDA(launch_mp_finalize(h->w, h->w, h->w.excl, P, I, st));
   if (inert) memcpy(inert, h->inert.data(), h->inert.size());
   h->st = st;
   return ok();
@@ -740,6 +763,40 @@ skmp_status mp_selfjoin(const void* R, int32_t k, int64_t n, int64_t ld, int32_t
   if (s == SKMP_OK) s = mp_finalize(h, P, I, inert, stream);
   mp_free(h);
   return s;
+}
+
+skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, int64_t nB, int64_t ldB,
+                      int32_t k, int32_t dtype, const skmp_mp_cfg* cfg, void* PA, int64_t* IA, void* PB,
+                      int64_t* IB, uint8_t* inert, void* stream) {
+  if (!PA || !IA || (PB && !IB) || (!PB && IB)) return set_error(SKMP_E_INVALID_ARG, "mp_abjoin: NULL output");
+  int ex = 0;
+  skmp_status s = mp_validate(RA, k, nA, ldA, dtype, cfg, &ex, true);
+  if (s) return s;
+  if ((s = mp_validate(RB, k, nB, ldB, dtype, cfg, &ex, true)) != SKMP_OK) return s;
+  skmp_mp *a = nullptr, *b = nullptr;
+  if ((s = mp_create_impl(RA, k, nA, ldA, dtype, cfg, stream, &a, true)) != SKMP_OK) return s;
+  if ((s = mp_create_impl(RB, k, nB, ldB, dtype, cfg, stream, &b, true)) != SKMP_OK) {
+    mp_free(a);
+    return s;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // pass 1: rows = test windows i, columns = train windows j = i + delta, delta in [0, n_subB)
+  // pass 2: rows = train windows j, columns = test windows i = j + delta, delta in [1, n_subA)
+  s = join_band(a->w, b->w, 0, b->w.n_sub, st);
+  if (s == SKMP_OK) s = join_band(b->w, a->w, 1, a->w.n_sub, st);
+  if (s == SKMP_OK) {
+    cudaError_t e = launch_mp_finalize(a->w, b->w, -1, PA, IA, st);
+    if (e == cudaSuccess && PB) e = launch_mp_finalize(b->w, a->w, -1, PB, IB, st);
+    if (e != cudaSuccess) s = cuda_error(e, "mp_abjoin: finalize");
+  }
+  if (s == SKMP_OK && inert) {
+    // reading 6 for an AB-join: a group is inert when both its test and train sketch series
+    // are entirely flat (an empty group)
+    for (int g = 0; g < k; ++g) inert[g] = a->inert[(size_t)g] && b->inert[(size_t)g];
+  }
+  mp_free(a);
+  mp_free(b);
+  return s == SKMP_OK ? ok() : s;
 }
 
 // ============================================================================================

@@ -59,6 +59,12 @@ inline int join_span(int dtype) {
   if (dtype == SKMP_F32 && join_x2_enabled()) return join_x2_span();
   return dtype == SKMP_F64 ? kJoinD64 : join_d32();
 }
+// rows of a diagonal block whose smallest diagonal is dmin: cells (i, i + delta) need
+// i < n_sub_r and i + delta < n_sub_c
+inline __host__ __device__ int64_t tile_rows(int64_t n_sub_r, int64_t n_sub_c, int64_t dmin) {
+  const int64_t a = n_sub_c - dmin;
+  return a < n_sub_r ? a : n_sub_r;
+}
 // FP32 profile keys store (candidate-set base + kKeyArgBias) so that bases down to -(D-1) fit
 constexpr int64_t kKeyArgBias = 32;
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
@@ -117,14 +123,19 @@ struct MpDev {
 };
 cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st);
 cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
-// band join: tiles described by blocks of W diagonals [dlo, dhi)
-cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
-                           int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
+// band join of row series w against column series wc (the same workspace for a self-join):
+// cells (i, i + delta), delta in [dlo, dhi), tiles described by blocks of W diagonals
+cudaError_t launch_mp_join(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi,
+                           const int64_t* d_tile_prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
+                           cudaStream_t st);
 // packed f32x2 FP32 join (mp_join_x2.cu), the default FP32 join
-cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_tile_prefix,
-                              int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st);
+cudaError_t launch_mp_join_x2(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi,
+                              const int64_t* d_tile_prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
+                              cudaStream_t st);
 cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);
-cudaError_t launch_mp_finalize(const MpDev& w, void* P, int64_t* I, cudaStream_t st);
+// rows of w resolved against neighbours in wo (self-join: wo = w, excl >= 0; AB-join: excl = -1)
+cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* P, int64_t* I,
+                               cudaStream_t st);
 
 // ------------------------------------------------------------------------------------------
 // detection (K8) — detect.cu

@@ -32,8 +32,11 @@ template <> struct JT<double> {
   static constexpr int D = kJoinD64;
 };
 
+// Row side = the series whose windows index the rows i; column side = the series of the
+// columns j = i + delta (the same series for a self-join; train/test for an AB-join pass).
+// Cell (i, j) exists iff i < n_sub and j < n_sub_c.
 struct JoinArgs {
-  const void* R;
+  const void* R;    // row side: series, prepared records, window means, profile keys
   int64_t ld;
   const void* Q;
   const double* mu;
@@ -41,6 +44,14 @@ struct JoinArgs {
   int64_t* keys;
   int64_t n_sub;
   int64_t n;
+  const void* Rc;   // column side
+  int64_t ldc;
+  const void* Qc;
+  const double* muc;
+  int64_t ldqc;
+  int64_t* keysc;
+  int64_t n_sub_c;
+  int64_t nc;
   int m;
   int L;
   int64_t dlo, dhi;
@@ -48,6 +59,35 @@ struct JoinArgs {
   int64_t nblk;
   int64_t blk0;
 };
+
+inline JoinArgs make_join_args(const MpDev& wr, const MpDev& wc, int64_t dlo, int64_t dhi,
+                               const int64_t* prefix, int64_t nblk, int64_t blk0) {
+  JoinArgs a;
+  a.R = wr.R;
+  a.ld = wr.ld;
+  a.Q = wr.Q;
+  a.mu = wr.mu;
+  a.ldq = wr.ldq;
+  a.keys = wr.keys;
+  a.n_sub = wr.n_sub;
+  a.n = wr.n;
+  a.Rc = wc.R;
+  a.ldc = wc.ld;
+  a.Qc = wc.Q;
+  a.muc = wc.mu;
+  a.ldqc = wc.ldq;
+  a.keysc = wc.keys;
+  a.n_sub_c = wc.n_sub;
+  a.nc = wc.n;
+  a.m = wr.m;
+  a.L = wr.L;
+  a.dlo = dlo;
+  a.dhi = dhi;
+  a.prefix = prefix;
+  a.nblk = nblk;
+  a.blk0 = blk0;
+  return a;
+}
 
 // ---- key encodings ------------------------------------------------------------------------
 __device__ __forceinline__ int32_t ord32(float f) {
@@ -178,7 +218,7 @@ __device__ __forceinline__ void decode_tile(const JoinArgs& a, int64_t W, int64_
   const int64_t rt = tile - a.prefix[b];
   *delta0 = (a.blk0 + b) * W;
   const int64_t dmin = *delta0 > a.dlo ? *delta0 : a.dlo;
-  const int64_t rows = a.n_sub - dmin;
+  const int64_t rows = tile_rows(a.n_sub, a.n_sub_c, dmin);
   *i0 = rt * a.L;
   *i1 = (*i0 + a.L < rows) ? *i0 + a.L : rows;
 }

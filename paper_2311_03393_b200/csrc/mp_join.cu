@@ -46,7 +46,7 @@ using namespace join;
 // smallest index of the candidate's D-cell set (see mp_final.cu): row i's cells in this thread
 // are j in [i + dt, i + dt + D), column c's cells are i in [c - dt - D + 1, c - dt].
 template <typename T, int D>
-SKMP_PUB_ATTR void publish_pair(int64_t* keys, typename JT<T>::Q* rowq, T* cthr, int rb_u,
+SKMP_PUB_ATTR void publish_pair(int64_t* keys, int64_t* keysc, typename JT<T>::Q* rowq, T* cthr, int rb_u,
                                           int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
                                           T colv0, T colv1) {
   if (rowa >= rowq[rb_u].w) {
@@ -58,11 +58,11 @@ SKMP_PUB_ATTR void publish_pair(int64_t* keys, typename JT<T>::Q* rowq, T* cthr,
     rowq[rb_u + 1].w = rowb;
   }
   if (colv0 >= cthr[ct0]) {
-    publish(keys, i_u + dt, colv0, i_u - (D - 1));
+    publish(keysc, i_u + dt, colv0, i_u - (D - 1));
     cthr[ct0] = colv0;
   }
   if (colv1 >= cthr[ct1]) {
-    publish(keys, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
+    publish(keysc, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
     cthr[ct1] = colv1;
   }
 }
@@ -101,7 +101,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
                                          const typename JT<T>::Q* ring1,
                                          const T* cth0, typename JT<T>::Q* rowq, T* cthr, int rb, int qt,
                                          int64_t ib, int64_t dt, const int (&lim)[D],
-                                         int64_t* keys) {
+                                         int64_t* keys, int64_t* keysc) {
   using Q = typename JT<T>::Q;
 #pragma unroll
   for (int u = 0; u < D; u += 2) {
@@ -152,7 +152,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
                      (colv1 >= cth0[((u + 1) % D) * RSD]);
     if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
-      publish_pair<T, D>(keys, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+      publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
                          ib + u, dt, rowa, rowb, colv0, colv1);
     }
   }
@@ -171,9 +171,12 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   T* cthr = reinterpret_cast<T*>(rowq + 2 * C);
 
   const int tid = threadIdx.x;
-  const int64_t n_sub = a.n_sub;
+  const int64_t n_sub = a.n_sub, n_sub_c = a.n_sub_c;  // rows: i < n_sub; columns: j < n_sub_c
+  constexpr int words = sizeof(T) == 4 ? 1 : 2;
   const Q* q = static_cast<const Q*>(a.Q) + (int64_t)g * a.ldq;
-  int64_t* keys = a.keys + (int64_t)g * n_sub * (sizeof(T) == 4 ? 1 : 2);
+  const Q* qc = static_cast<const Q*>(a.Qc) + (int64_t)g * a.ldqc;
+  int64_t* keys = a.keys + (int64_t)g * n_sub * words;
+  int64_t* keysc = a.keysc + (int64_t)g * n_sub_c * words;
   const int64_t dt = delta0 + (int64_t)tid * D;  // this thread's first diagonal
 
   // per-slot validity limit: cell (i, i+dt+d) is valid iff i < lim[d]
@@ -181,7 +184,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     const int64_t dd = dt + d;
-    lim[d] = (dd >= a.dlo && dd < a.dhi && dd < n_sub) ? (int)(n_sub - dd) : 0;
+    lim[d] = (dd >= a.dlo && dd < a.dhi && dd < n_sub_c) ? (int)tile_rows(n_sub, n_sub_c, dd) : 0;
   }
   // diagonals cut by the band edges: every chunk of this tile needs the per-cell mask
   const bool diag_masked = (delta0 < a.dlo) || (delta0 + W > a.dhi);
@@ -190,25 +193,26 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   T cov[D];
   {
     const T* R = static_cast<const T*>(a.R) + (int64_t)g * a.ld;
+    const T* Rc = static_cast<const T*>(a.Rc) + (int64_t)g * a.ldc;
     const double mua = a.mu[(int64_t)g * a.ldq + i0];
     double mub[D], acc[D], w[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int64_t j = i0 + dt + d;
-      mub[d] = (j < n_sub) ? a.mu[(int64_t)g * a.ldq + j] : 0.0;
+      mub[d] = (j < n_sub_c) ? a.muc[(int64_t)g * a.ldqc + j] : 0.0;
       acc[d] = 0.0;
     }
     const int64_t jb = i0 + dt;
 #pragma unroll
-    for (int d = 0; d < D - 1; ++d) w[d] = (jb + d < a.n) ? (double)R[jb + d] : 0.0;
+    for (int d = 0; d < D - 1; ++d) w[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
     for (int s0 = 0; s0 < a.m; s0 += D) {
 #pragma unroll
       for (int e = 0; e < D; ++e) {
         const int s = s0 + e;
         if (s < a.m) {
           const int64_t t = jb + s + D - 1;
-          w[(e + D - 1) % D] = (t < a.n) ? (double)R[t] : 0.0;
-          const double av = (double)R[i0 + s] - mua;
+          w[(e + D - 1) % D] = (t < a.nc) ? (double)Rc[t] : 0.0;
+          const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
 #pragma unroll
           for (int d = 0; d < D; ++d) acc[d] = fma(av, w[(e + d) % D] - mub[d], acc[d]);
         }
@@ -217,7 +221,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     const Q qi = q[i0];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const Q qj = q[i0 + dt + d];  // padded: safe past n_sub
+      const Q qj = qc[i0 + dt + d];  // padded: safe past n_sub_c
       const double adj = (double)qi.x * (double)qj.y + (double)qj.x * (double)qi.y;
       cov[d] = (T)(acc[d] - adj);
     }
@@ -226,8 +230,8 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // ---- prologue: stage rows [i0, i0+C) and ring columns [i0+delta0, i0+delta0+W+C) ----------
   for (int e = tid; e < W + C; e += NT) {
     const int64_t c = i0 + delta0 + e;
-    stage_q<T>(&ring[G::pos(c)], &q[c]);
-    cthr[G::pos(c)] = (c < n_sub) ? load_thr(keys, c, (T*)nullptr) : pos_inf<T>();
+    stage_q<T>(&ring[G::pos(c)], &qc[c]);
+    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
   }
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
@@ -264,8 +268,8 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #pragma unroll
       for (int e = 0; e < CPT; ++e) {
         const int64_t nc = r + delta0 + W + C + tid + e * NT;
-        stage_q<T>(&ring[G::pos(nc)], &q[nc]);
-        nthr_c[e] = (nc < n_sub) ? load_thr(keys, nc, (T*)nullptr) : pos_inf<T>();
+        stage_q<T>(&ring[G::pos(nc)], &qc[nc]);
+        nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) : pos_inf<T>();
         const int64_t nr = r + C + tid + e * NT;
         stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
         nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) : pos_inf<T>();
@@ -277,17 +281,17 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     const int nrot = (int)((rend - r) / D);
     int rb = (int)(r & (2 * C - 1));
     int64_t ib = r;
-    // the chunk needs per-cell masks only where it reaches the triangle edge (i + delta >= n_sub)
-    // or the band's diagonal edges
-    const bool cmasked = MASKED && (diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub);
+    // the chunk needs per-cell masks only where it reaches the triangle / rectangle edges
+    // (i + delta >= n_sub_c, i >= n_sub) or the band's diagonal edges
+    const bool cmasked = MASKED && (diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub_c || rend > n_sub);
     for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
         rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
-                                  rowq, cthr, rb, qt, ib, dt, lim, keys);
+                                  rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       else
         rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
-                                   rowq, cthr, rb, qt, ib, dt, lim, keys);
+                                   rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       qt = qt1;
       rb = (rb + D) & (2 * C - 1);
     }
@@ -311,7 +315,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int x = 0; x < D - 1; ++x) {
     const T v = CK[x];
     const int64_t c = i1 + dt + x;
-    if (c < n_sub && v >= cthr[G::pos(c)]) publish(keys, c, v, c - dt - (D - 1));
+    if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v, c - dt - (D - 1));
   }
 }
 
@@ -337,7 +341,7 @@ join_kernel(JoinArgs a) {
     const int64_t rt = tile - a.prefix[b];
     const int64_t delta0 = (a.blk0 + b) * W;
     const int64_t dmin = delta0 > a.dlo ? delta0 : a.dlo;
-    const int64_t rows = a.n_sub - dmin;
+    const int64_t rows = tile_rows(a.n_sub, a.n_sub_c, dmin);
     const int64_t i0 = rt * a.L;
     const int64_t i1 = (i0 + a.L < rows) ? i0 + a.L : rows;
     s_tile[0] = delta0;
@@ -346,34 +350,17 @@ join_kernel(JoinArgs a) {
   }
   __syncthreads();
   const int64_t delta0 = s_tile[0], i0 = s_tile[1], i1 = s_tile[2];
-  // rows are processed in whole D-row rotations; rows beyond i1 are masked cells
+  // rows are processed in whole D-row rotations; rows beyond the edges are masked cells
   const int64_t i1r = i0 + (((i1 - i0) + D - 1) / D) * D;
-  const bool masked = (delta0 < a.dlo) || (delta0 + W > a.dhi) || (i1r - 1 + delta0 + W - 1 >= a.n_sub);
-  (void)masked;  // masking is decided per chunk inside the tile
   join_tile<T, D, NT, C, true>(a, g, delta0, i0, i1r, smem_raw);
 }
 
 template <typename T, int D>
-cudaError_t launch_join_t(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* prefix,
+cudaError_t launch_join_t(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi, const int64_t* prefix,
                           int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
   constexpr int NT = kJoinNT, C = kJoinC;
   using G = Geo<T, D, NT, C>;
-  JoinArgs a;
-  a.R = w.R;
-  a.ld = w.ld;
-  a.Q = w.Q;
-  a.mu = w.mu;
-  a.ldq = w.ldq;
-  a.keys = w.keys;
-  a.n_sub = w.n_sub;
-  a.n = w.n;
-  a.m = w.m;
-  a.L = w.L;
-  a.dlo = dlo;
-  a.dhi = dhi;
-  a.prefix = prefix;
-  a.nblk = nblk;
-  a.blk0 = blk0;
+  const JoinArgs a = make_join_args(w, wc, dlo, dhi, prefix, nblk, blk0);
   const size_t smem = G::smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(join_kernel<T, D, NT, C>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -395,16 +382,16 @@ int join_d32() {
   return d;
 }
 
-cudaError_t launch_mp_join(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* d_prefix,
-                           int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
+cudaError_t launch_mp_join(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi,
+                           const int64_t* d_prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
+                           cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
   if (w.dtype == SKMP_F32) {
-    if (join_x2_enabled())
-      return launch_mp_join_x2(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
-    if (join_d32() == 16) return launch_join_t<float, 16>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
-    return launch_join_t<float, 8>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+    if (join_x2_enabled()) return launch_mp_join_x2(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+    if (join_d32() == 16) return launch_join_t<float, 16>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+    return launch_join_t<float, 8>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
   }
-  return launch_join_t<double, kJoinD64>(w, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
+  return launch_join_t<double, kJoinD64>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
 }
 
 }  // namespace skmp

@@ -102,7 +102,8 @@ __device__ __forceinline__ int pos(int64_t c) {
 
 // masking limits of a thread's diagonals relative to dt (3 registers instead of 2 DG)
 struct Lim {
-  int lo, hi, edge;
+  int lo, hi, edge;  // diagonal band [lo, hi) and column edge, relative to dt
+  int rows;          // row edge: i < rows (AB-join passes; = n_sub for a self-join)
 };
 
 // per-slot operand registers
@@ -114,7 +115,7 @@ struct Col {
 // smallest index of the winning D-cell set (resolved exactly in mp_final.cu): a row's set is one
 // group's DG diagonals of this thread (group B when its maximum is strictly larger: ties go to
 // the smaller indices of group A), a column's set is the DG rows it spent in this thread.
-SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int ctA1,
+SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, int64_t* keysc, Smem* sm, int rbu, int ctA0, int ctA1,
                                         int64_t i_u, int64_t dt, float rowaA, float rowaB,
                                         float rowbA, float rowbB, float cA0, float cA1, float cB0,
                                         float cB1) {
@@ -129,19 +130,19 @@ SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, Smem* sm, int rbu, int ctA0, int
   }
   // columns c = i + dt (A) and c + H (B) complete after row i: their rows are [i - DG + 1, i]
   if (cA0 >= sm->thrA[ctA0]) {
-    publish(keys, i_u + dt, cA0, i_u - (DG - 1));
+    publish(keysc, i_u + dt, cA0, i_u - (DG - 1));
     sm->thrA[ctA0] = cA0;
   }
   if (cA1 >= sm->thrA[ctA1]) {
-    publish(keys, i_u + 1 + dt, cA1, i_u + 1 - (DG - 1));
+    publish(keysc, i_u + 1 + dt, cA1, i_u + 1 - (DG - 1));
     sm->thrA[ctA1] = cA1;
   }
   if (cB0 >= sm->thrB[ctA0]) {
-    publish(keys, i_u + dt + H, cB0, i_u - (DG - 1));
+    publish(keysc, i_u + dt + H, cB0, i_u - (DG - 1));
     sm->thrB[ctA0] = cB0;
   }
   if (cB1 >= sm->thrB[ctA1]) {
-    publish(keys, i_u + 1 + dt + H, cB1, i_u + 1 - (DG - 1));
+    publish(keysc, i_u + 1 + dt + H, cB1, i_u + 1 - (DG - 1));
     sm->thrB[ctA1] = cB1;
   }
 }
@@ -164,8 +165,9 @@ __device__ __forceinline__ void row_keys(int u, f2 (&cov)[DG], const Col (&X)[DG
   if (MASKED) {
 #pragma unroll
     for (int d = 0; d < DG; ++d) {
-      ka[d] = (d >= lim.lo && d < lim.hi && irow + d < lim.edge) ? ka[d] : neg_inf<float>();
-      kb[d] = (d >= lim.lo - H && d < lim.hi - H && irow + d < lim.edge - H) ? kb[d] : neg_inf<float>();
+      ka[d] = (d >= lim.lo && d < lim.hi && irow + d < lim.edge && irow < lim.rows) ? ka[d] : neg_inf<float>();
+      kb[d] = (d >= lim.lo - H && d < lim.hi - H && irow + d < lim.edge - H && irow < lim.rows) ? kb[d]
+                                                                                                 : neg_inf<float>();
     }
   }
 }
@@ -183,7 +185,7 @@ template <bool MASKED>
 __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (&CA)[DG], float (&CB)[DG],
                                             Smem* sm, int rb, int qt, int qt1, int64_t ib, int64_t dt,
                                             const Lim& lim,
-                                            int64_t* keys) {
+                                            int64_t* keys, int64_t* keysc) {
 #pragma unroll
   for (int u = 0; u < DG; u += 2) {
     // -- row u: its entering column (slot DG-1) takes the register of the column completed at u-1
@@ -219,7 +221,7 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (
     const bool hit = (rowa >= sm->rthr[rb + u]) | (rowb >= sm->rthr[rb + u + 1]) | (cA0 >= sm->thrA[t0]) |
                      (cA1 >= sm->thrA[t1]) | (cB0 >= sm->thrB[t0]) | (cB1 >= sm->thrB[t1]);
     if (__any_sync(0xffffffffu, hit))
-      publish_x2(keys, sm, rb + u, t0, t1, ib + u, dt, rowaA, rowaB, rowbA, rowbB, cA0, cA1, cB0, cB1);
+      publish_x2(keys, keysc, sm, rb + u, t0, t1, ib + u, dt, rowaA, rowaB, rowbA, rowbB, cA0, cA1, cB0, cB1);
   }
 }
 
@@ -266,14 +268,15 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 // next chunk's column record c (and c + H) and row i: raw copies + key high words (the
 // orderable rho of the current best; a possibly stale L1 copy only costs an extra publish)
-__device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int64_t* keys, int64_t c,
-                                           int64_t i, int64_t n_sub, int e) {
-  cp_async16(&sm->rawA[e], q + c);
-  cp_async16(&sm->rawB[e], q + c + H);
+__device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int64_t* keys, const float4* qc,
+                                           const int64_t* keysc, int64_t c, int64_t i, int64_t n_sub,
+                                           int64_t n_sub_c, int e) {
+  cp_async16(&sm->rawA[e], qc + c);
+  cp_async16(&sm->rawB[e], qc + c + H);
   cp_async16(&sm->rawR[e], q + i);
   const int32_t inf = 0x7f800000;  // orderable(+inf): never beaten
-  if (c < n_sub) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keys + c) + 4); else sm->rawtA[e] = inf;
-  if (c + H < n_sub) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keys + c + H) + 4); else sm->rawtB[e] = inf;
+  if (c < n_sub_c) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keysc + c) + 4); else sm->rawtA[e] = inf;
+  if (c + H < n_sub_c) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keysc + c + H) + 4); else sm->rawtB[e] = inf;
   if (i < n_sub) cp_async4(&sm->rawtR[e], reinterpret_cast<const char*>(keys + i) + 4); else sm->rawtR[e] = inf;
 }
 __device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e) {
@@ -302,9 +305,11 @@ join_x2_kernel(JoinArgs a) {
   const int64_t delta0 = s_tile[0], i0 = s_tile[1];
   const int64_t i1 = i0 + ((s_tile[2] - i0 + DG - 1) / DG) * DG;  // whole rotations; tail masked
   const int tid = threadIdx.x;
-  const int64_t n_sub = a.n_sub;
+  const int64_t n_sub = a.n_sub, n_sub_c = a.n_sub_c;  // rows i < n_sub, columns j < n_sub_c
   const float4* q = static_cast<const float4*>(a.Q) + (int64_t)g * a.ldq;
+  const float4* qc = static_cast<const float4*>(a.Qc) + (int64_t)g * a.ldqc;
   int64_t* keys = a.keys + (int64_t)g * n_sub;
+  int64_t* keysc = a.keysc + (int64_t)g * n_sub_c;
   const int64_t dt = delta0 + (int64_t)tid * DG;
 
   // cell (i, i + dt + d) of group A is valid iff lo <= d < hi and i + d < edge (group B: d + H)
@@ -314,7 +319,8 @@ join_x2_kernel(JoinArgs a) {
     auto clampi = [&](int64_t v) { return (int)(v < -big ? -big : (v > big ? big : v)); };
     lim.lo = clampi(a.dlo - dt);
     lim.hi = clampi(a.dhi - dt);
-    lim.edge = clampi(n_sub - dt);
+    lim.edge = clampi(n_sub_c - dt);
+    lim.rows = clampi(n_sub);
   }
   const bool diag_masked = (delta0 < a.dlo) || (delta0 + W > a.dhi);
 
@@ -322,21 +328,23 @@ join_x2_kernel(JoinArgs a) {
   f2 cov[DG];
   {
     const float* R = static_cast<const float*>(a.R) + (int64_t)g * a.ld;
+    const float* Rc = static_cast<const float*>(a.Rc) + (int64_t)g * a.ldc;
     const double* mu = a.mu + (int64_t)g * a.ldq;
+    const double* muc = a.muc + (int64_t)g * a.ldqc;
     const double mua = mu[i0];
     double acc[2 * DG], mub[2 * DG];
 #pragma unroll
     for (int e = 0; e < 2 * DG; ++e) {
       const int64_t j = i0 + dt + (e % DG) + (e >= DG ? H : 0);
-      mub[e] = (j < n_sub) ? mu[j] : 0.0;
+      mub[e] = (j < n_sub_c) ? muc[j] : 0.0;
       acc[e] = 0.0;
     }
     for (int s = 0; s < a.m; ++s) {
-      const double av = (double)R[i0 + s] - mua;
+      const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
 #pragma unroll
       for (int e = 0; e < 2 * DG; ++e) {
         const int64_t t = i0 + dt + (e % DG) + (e >= DG ? H : 0) + s;
-        const double bv = (t < a.n) ? (double)R[t] : 0.0;
+        const double bv = (t < a.nc) ? (double)Rc[t] : 0.0;
         acc[e] = fma(av, bv - mub[e], acc[e]);
       }
     }
@@ -344,7 +352,7 @@ join_x2_kernel(JoinArgs a) {
     float c32[2 * DG];
 #pragma unroll
     for (int e = 0; e < 2 * DG; ++e) {
-      const float4 qj = q[i0 + dt + (e % DG) + (e >= DG ? H : 0)];  // padded: safe past n_sub
+      const float4 qj = qc[i0 + dt + (e % DG) + (e >= DG ? H : 0)];  // padded: safe past n_sub_c
       const double adj = (double)qi.x * (double)qj.y + (double)qj.x * (double)qi.y;
       c32[e] = (float)(acc[e] - adj);
     }
@@ -355,7 +363,7 @@ join_x2_kernel(JoinArgs a) {
   // ---- prologue: records [i0+delta0, i0+delta0+H+C), rows [i0, i0+C) ------------------------
   for (int e = tid; e < H + C; e += NT) {
     ColStage cs;
-    fetch_col(cs, q, keys, i0 + delta0 + e, n_sub);
+    fetch_col(cs, qc, keysc, i0 + delta0 + e, n_sub_c);
     land_col(cs, &sm, i0 + delta0 + e);
   }
   {
@@ -376,17 +384,17 @@ join_x2_kernel(JoinArgs a) {
   for (int64_t r = i0; r < i1; r += C) {
     const int64_t rend = (r + C < i1) ? r + C : i1;
     const bool more = r + C < i1;
-    if (more) stage_next(&sm, q, keys, r + delta0 + H + C + tid, r + C + tid, n_sub, tid);
+    if (more) stage_next(&sm, q, keys, qc, keysc, r + delta0 + H + C + tid, r + C + tid, n_sub, n_sub_c, tid);
     const int nrot = (int)((rend - r) / DG);
     int rb = (int)(r & (2 * C - 1));
     int64_t ib = r;
-    const bool cmasked = diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub;
+    const bool cmasked = diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub_c || rend > n_sub;
     for (int it = 0; it < nrot; ++it, ib += DG) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys);
+        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys, keysc);
       else
-        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys);
+        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys, keysc);
       qt = qt1;
       rb = (rb + DG) & (2 * C - 1);
     }
@@ -402,8 +410,8 @@ join_x2_kernel(JoinArgs a) {
   for (int x = 0; x < DG - 1; ++x) {
     const int64_t c = i1 + dt + x;
     const int e = pos(c);
-    if (c < n_sub && CA[x] >= sm.thrA[e]) publish(keys, c, CA[x], c - dt - (DG - 1));
-    if (c + H < n_sub && CB[x] >= sm.thrB[e]) publish(keys, c + H, CB[x], c - dt - (DG - 1));
+    if (c < n_sub_c && CA[x] >= sm.thrA[e]) publish(keysc, c, CA[x], c - dt - (DG - 1));
+    if (c + H < n_sub_c && CB[x] >= sm.thrB[e]) publish(keysc, c + H, CB[x], c - dt - (DG - 1));
   }
 }
 
@@ -421,24 +429,10 @@ bool join_x2_enabled() {
   return on;
 }
 
-cudaError_t launch_mp_join_x2(const MpDev& w, int64_t dlo, int64_t dhi, const int64_t* prefix,
-                              int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
-  JoinArgs a;
-  a.R = w.R;
-  a.ld = w.ld;
-  a.Q = w.Q;
-  a.mu = w.mu;
-  a.ldq = w.ldq;
-  a.keys = w.keys;
-  a.n_sub = w.n_sub;
-  a.n = w.n;
-  a.m = w.m;
-  a.L = w.L;
-  a.dlo = dlo;
-  a.dhi = dhi;
-  a.prefix = prefix;
-  a.nblk = nblk;
-  a.blk0 = blk0;
+cudaError_t launch_mp_join_x2(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi,
+                              const int64_t* prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
+                              cudaStream_t st) {
+  const JoinArgs a = make_join_args(w, wc, dlo, dhi, prefix, nblk, blk0);
   dim3 grid((unsigned)ntiles, (unsigned)w.k);
   join_x2_kernel<<<grid, NT, 0, st>>>(a);
   count_launches(1);

@@ -18,8 +18,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (F32, F64, Sketch, mp_band, mp_create, mp_finalize, mp_join, mp_keys, sketch_refresh,
-               sketch_view64)
+from . import (F32, F64, Sketch, detect_dimension, mp_band, mp_create, mp_finalize, mp_join, mp_keys,
+               sketch_refresh, sketch_view64)
 
 INT64_MIN = -(1 << 63)
 
@@ -76,3 +76,24 @@ def mp_selfjoin_dist(R: torch.Tensor, m: int, *, excl: int = -1, reseed_rows: in
         out = mp_finalize(w)
     w.free()
     return out
+
+
+def detect_dimension_dist(sk: Sketch, sources, t: int, g: int, m: int, device, group=None):
+    """Alg. 3 with the streams sharded over ranks (each rank's sketch plan holds its own shard):
+    every rank scores its members of J_g (discord_dims), then the (score, plan order) maxima are
+    all-gathered and every rank returns the same (id*, score, nn).  Ranks hold contiguous id
+    shards, so (rank, local order) is the global plan order of Alg. 3's scan."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    loc = detect_dimension(sk, sources, t, g, m)
+    row = torch.tensor([-1.0, 0.0, 0.0, 0.0], dtype=torch.float64, device=device) if loc is None else \
+        torch.tensor([1.0, loc[1], float(loc[0]), float(loc[2])], dtype=torch.float64, device=device)
+    allr = [torch.empty_like(row) for _ in range(world)]
+    dist.all_gather(allr, row, group=group)
+    best = None
+    for r in range(world):
+        ok, sc, j, nn = (float(x) for x in allr[r].tolist())
+        if ok > 0 and (best is None or sc > best[1]):  # strict: the earliest rank wins ties
+            best = (int(j), sc, int(nn))
+    return best
+
