@@ -13,7 +13,9 @@ FP32, 20 injected discords):
   f2     discord_dims over the top discord's group (Alg. 3 dimension detection)
 Multi-GPU (torchrun, N>1): streams are sharded over ranks, partial sketches are sum-all-reduced
 (NCCL), each rank joins its diagonal band (mp_band) and the profile keys are max-all-reduced
-(NCCL); rank 0 finalizes and ranks the discords.  Strong scaling (fixed total work).
+(NCCL); every rank finalizes a slice of the windows (reduced to rank 0), rank 0 ranks the
+discords, and Alg. 3 runs on every rank's own streams of the group (all-gathered maxima).
+Strong scaling (fixed total work).
 
 `value` = exact join cells per step (k (n_sub-r-1)(n_sub-r)/2) / device step time, inputs
 resident in HBM.  `e2e` = the same with the inputs in pinned HOST memory handed to the C-ABI
@@ -275,8 +277,12 @@ def main():
             keys, words = skmp.mp_keys(w)
             sdist.reduce_keys(keys, words)
         res = None
+        if world > 1:  # every rank resolves a slice of the windows, P / I reduced to rank 0
+            fin = sdist.finalize_dist(w)
+        else:
+            fin = skmp.mp_finalize(w)
         if rank == 0:
-            P, I, inert = skmp.mp_finalize(w)
+            P, I, inert = fin
             res = skmp.discord_topk(P, I, inert, m=m, top=top)
         w.free()
         if e: e[5].record()

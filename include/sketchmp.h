@@ -192,6 +192,11 @@ int32_t mp_tile_width(int32_t dtype);
  * Requires the full diagonal range to have been joined.  Synchronous only for the inert copy.
  * Errors: INVALID_ARG, CUDA. */
 skmp_status mp_finalize(skmp_mp* w, void* P, int64_t* I, uint8_t* inert, void* stream);
+/* Finalize only the windows [row_lo, row_hi) of every series (0 <= row_lo <= row_hi <= n_sub)
+ * into the full-size P / I (other entries untouched): the multi-GPU path shards the finalize
+ * over ranks after the key reduce.  Same semantics and errors as mp_finalize. */
+skmp_status mp_finalize_rows(skmp_mp* w, int64_t row_lo, int64_t row_hi, void* P, int64_t* I,
+                             uint8_t* inert, void* stream);
 void mp_free(skmp_mp* w);
 
 /* One-shot: mp_create + mp_join(all) + mp_finalize + mp_free. */

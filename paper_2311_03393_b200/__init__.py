@@ -4,7 +4,8 @@ Argument marshalling only: every step of the path runs in libsketchmp.so's CUDA 
 PyTorch supplies device memory and the current CUDA stream.  The same names as the C-ABI:
 
     sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
-    sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize, mp_free,
+    sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize,
+    mp_finalize_rows, mp_free,
     mp_selfjoin, mp_abjoin, discord_topk, discord_dims
 
 There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
@@ -79,6 +80,7 @@ _SIGS = {
     "mp_tile_width": (_I32, [_I32]),
     "mp_band": (ctypes.c_int, [_I64, _I32, _I32, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "mp_finalize": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "mp_finalize_rows": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _P, _P]),
     "mp_free": (None, [_P]),
     "mp_selfjoin": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
     "discord_topk": (ctypes.c_int, [_P, _P, _P, _I32, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _P, _P,
@@ -357,6 +359,20 @@ def mp_finalize(w: MpWorkspace, P=None, I=None, stream=None):
         I = torch.empty((w.k, w.n_sub), dtype=torch.int64, device="cuda")
     inert = np.zeros(w.k, dtype=np.uint8)
     _check(lib().mp_finalize(w.handle, _ptr(P), _ptr(I), _ptr(inert), _stream(stream)))
+    return P, I, inert.astype(bool)
+
+
+def mp_finalize_rows(w: MpWorkspace, row_lo: int, row_hi: int, P=None, I=None, stream=None):
+    """Finalize windows [row_lo, row_hi) of every series into P / I (allocated zero-filled when
+    not given, so per-rank slices can be sum-reduced)."""
+    import torch
+    tdt = torch.float32 if w.dtype == F32 else torch.float64
+    if P is None:
+        P = torch.zeros((w.k, w.n_sub), dtype=tdt, device="cuda")
+    if I is None:
+        I = torch.zeros((w.k, w.n_sub), dtype=torch.int64, device="cuda")
+    inert = np.zeros(w.k, dtype=np.uint8)
+    _check(lib().mp_finalize_rows(w.handle, row_lo, row_hi, _ptr(P), _ptr(I), _ptr(inert), _stream(stream)))
     return P, I, inert.astype(bool)
 
 

@@ -746,6 +746,18 @@ skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* s
   return ok();
 }
 
+skmp_status mp_finalize_rows(skmp_mp* h, int64_t row_lo, int64_t row_hi, void* P, int64_t* I,
+                             uint8_t* inert, void* stream) {
+  if (!h || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: NULL argument");
+  if (row_lo < 0 || row_hi < row_lo || row_hi > h->w.n_sub)
+    return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: need 0 <= row_lo <= row_hi <= n_sub");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SKMP_CUDA(launch_mp_finalize(h->w, h->w, h->w.excl, P, I, st, row_lo, row_hi));
+  if (inert) memcpy(inert, h->inert.data(), h->inert.size());
+  h->st = st;
+  return ok();
+}
+
 void mp_free(skmp_mp* h) {
   if (!h) return;
   if (h->w.flat_list) cudaFreeAsync(h->w.flat_list, h->st);

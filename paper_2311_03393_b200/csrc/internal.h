@@ -134,8 +134,9 @@ cudaError_t launch_mp_join_x2(const MpDev& w, const MpDev& wc, int64_t dlo, int6
                               cudaStream_t st);
 cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);
 // rows of w resolved against neighbours in wo (self-join: wo = w, excl >= 0; AB-join: excl = -1)
+// (rows [row_lo, row_hi) only; row_hi < 0 -> all rows)
 cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* P, int64_t* I,
-                               cudaStream_t st);
+                               cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1);
 
 // ------------------------------------------------------------------------------------------
 // detection (K8) — detect.cu

@@ -87,91 +87,65 @@ __device__ __forceinline__ bool admissible(int64_t i, int64_t j, int64_t n_sub_o
   return j >= 0 && j < n_sub_o && (excl < 0 || dj > excl);
 }
 
-// Nearest admissible member of the candidate set [b, b + SPAN) (windows of the other series wo)
-// of non-flat row i of w (-1 if none).
+// Window positions staged per warp and chunk: the row's window and the candidate windows
+// [b, b + SPAN - 1 + MC) are copied to shared memory with every load issued before any use (one
+// L2 round trip per chunk instead of one per dependent load), then read back conflict-free.
+// Staged values are converted to FP64 once (an FP32 -> FP64 conversion per use would cost
+// SPAN conversions per window position).
+template <typename T> struct FinChunk { static constexpr int MC = 256; };
+constexpr int kFinWarps = 8;  // rows (warps) per CTA
 template <typename T, int SPAN>
-__device__ __forceinline__ int64_t resolve_set(const MpDev& w, const MpDev& wo, int excl, int g, int64_t i,
-                                               int64_t b, int lane) {
+__host__ __device__ constexpr int fin_stride() { return 2 * FinChunk<T>::MC + SPAN; }  // doubles per warp
+
+// stage xi[s] = R[i + s0 + s] (s < len) and xo[t] = Ro[clamp(b + s0 + t)] (t < len + SPAN - 1)
+template <typename T, int SPAN>
+__device__ __forceinline__ void fin_stage(double* xi, double* xo, const T* R, const T* Ro, int64_t i, int64_t b,
+                                          int s0, int len, int64_t n_o, int lane) {
+  constexpr int MC = FinChunk<T>::MC;
+  constexpr int NI = MC / 32, NO = (MC + SPAN - 1 + 31) / 32;
+  T vi[NI], vo[NO];
+#pragma unroll
+  for (int q = 0; q < NI; ++q) {
+    const int s = lane + 32 * q;
+    vi[q] = s < len ? R[i + s0 + s] : (T)0;
+  }
+#pragma unroll
+  for (int q = 0; q < NO; ++q) {
+    const int t = lane + 32 * q;
+    int64_t idx = b + s0 + t;
+    idx = idx < 0 ? 0 : (idx >= n_o ? n_o - 1 : idx);  // only inadmissible members read clamped data
+    vo[q] = t < len + SPAN - 1 ? Ro[idx] : (T)0;
+  }
+#pragma unroll
+  for (int q = 0; q < NI; ++q) xi[lane + 32 * q] = (double)vi[q];
+#pragma unroll
+  for (int q = 0; q < NO; ++q)
+    if (lane + 32 * q < MC + SPAN - 1) xo[lane + 32 * q] = (double)vo[q];
+  __syncwarp();
+}
+
+// rows of w against neighbours in wo (wo = w for a self-join with exclusion radius excl >= 0;
+// an AB-join passes the other series and excl = -1).  One warp per row.
+template <typename T, int SPAN>
+__global__ void __launch_bounds__(32 * kFinWarps)
+finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
+                int64_t* __restrict__ I) {
   static_assert(SPAN <= 32 && (SPAN & (SPAN - 1)) == 0, "span must be a power of two <= 32");
+  constexpr int MC = FinChunk<T>::MC;
+  __shared__ double fsm[kFinWarps * fin_stride<T, SPAN>()];
+  const int lane = threadIdx.x & 31;
+  double* xi = fsm + (threadIdx.x >> 5) * fin_stride<T, SPAN>();
+  double* xo = xi + MC;
+  const int64_t i = row_lo + (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  const int g = blockIdx.y;
+  if (i >= row_hi) return;  // warp-uniform
+  const int words = (w.dtype == SKMP_F32) ? 1 : 2;
+  const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
   const int64_t o = (int64_t)g * w.ldq, oo = (int64_t)g * wo.ldq;
   const T* R = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
   const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
   const int m = w.m;
-  const double mi = w.mu[o + i];
-  const T* Rj[SPAN];
-#pragma unroll
-  for (int d = 0; d < SPAN; ++d) {
-    const int64_t j = b + d;
-    Rj[d] = Ro + (admissible(i, j, wo.n_sub, excl) ? j : 0);
-  }
-  double acc[SPAN], asum = 0.0;
-#pragma unroll
-  for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
-  // 4 window positions per lane per step, loads first: the data sits in L2 and a dependent
-  // load -> FMA chain per position would expose its latency
-  constexpr int U = 4;
-  for (int s0 = lane; s0 < m; s0 += 32 * U) {
-    T xa[U], xb[U][SPAN];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int s = s0 + 32 * u < m ? s0 + 32 * u : s0;  // clamped in range; masked below
-      xa[u] = R[i + s];
-#pragma unroll
-      for (int d = 0; d < SPAN; ++d) xb[u][d] = Rj[d][s];
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (s0 + 32 * u < m) {
-        const double a = (double)xa[u] - mi;
-        asum += a;
-#pragma unroll
-        for (int d = 0; d < SPAN; ++d) acc[d] = fma(a, (double)xb[u][d], acc[d]);
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
-  xsum<SPAN>(acc, lane);
-  int d = xidx<SPAN>(lane);
-  const int64_t j = b + d;
-  double dd = __longlong_as_double(0x7ff0000000000000ll);  // +inf: not admissible
-  if (admissible(i, j, wo.n_sub, excl)) {
-    if (wo.flat[oo + j]) {
-      dd = (double)m;  // reading 5: flat vs non-flat
-    } else {
-      // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i)
-      const double cov = acc[0] - wo.mu[oo + j] * asum;
-      dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + j]);
-    }
-  }
-  // warp argmin over the SPAN distinct lanes' (dd, d), smallest d on ties
-#pragma unroll
-  for (int q = 16; q >= 1; q >>= 1) {
-    const double od = __shfl_xor_sync(0xffffffffu, dd, q);
-    const int oi = __shfl_xor_sync(0xffffffffu, d, q);
-    if (od < dd || (od == dd && oi < d)) {
-      dd = od;
-      d = oi;
-    }
-  }
-  return dd < __longlong_as_double(0x7ff0000000000000ll) ? b + d : -1;
-}
-
-// rows of w against neighbours in wo (wo = w for a self-join with exclusion radius excl >= 0;
-// an AB-join passes the other series and excl = -1)
-template <typename T, int SPAN>
-__global__ void finalize_kernel(MpDev w, MpDev wo, int excl, T* __restrict__ P, int64_t* __restrict__ I) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int g = blockIdx.y;
-  if (row >= w.n_sub) return;
-  const int64_t i = row;
-  const int words = (w.dtype == SKMP_F32) ? 1 : 2;
-  const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
-  const int64_t o = (int64_t)g * w.ldq;
-  const int m = w.m;
   const double sqm = sqrt((double)m);
-  const int64_t oo = (int64_t)g * wo.ldq;
   const int32_t nf = wo.nflat[g];
   const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
   const bool fi = w.flat[o + i] != 0;
@@ -187,30 +161,80 @@ __global__ void finalize_kernel(MpDev w, MpDev wo, int excl, T* __restrict__ P, 
       p = sqm;  // every admissible neighbour is non-flat: the smallest one
       j = (excl < 0 || i - excl - 1 >= 0) ? 0 : i + excl + 1;
     }
+  } else if (!has) {
+    p = __longlong_as_double(0x7ff8000000000000ll);  // no candidate (band not covered)
+    j = -1;
   } else {
-    j = has ? resolve_set<T, SPAN>(w, wo, excl, g, i, j, lane) : -1;
+    // ---- resolve the winning set [b, b + SPAN): nearest admissible member (Def. 3) ----------
+    const int64_t b = j;
+    const double mi = w.mu[o + i];
+    double acc[SPAN], asum = 0.0;
+#pragma unroll
+    for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
+    for (int s0 = 0; s0 < m; s0 += MC) {
+      const int len = m - s0 < MC ? m - s0 : MC;
+      fin_stage<T, SPAN>(xi, xo, R, Ro, i, b, s0, len, wo.n, lane);
+      for (int s = lane; s < len; s += 32) {
+        const double a = xi[s] - mi;
+        asum += a;
+#pragma unroll
+        for (int d = 0; d < SPAN; ++d) acc[d] = fma(a, xo[s + d], acc[d]);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+    xsum<SPAN>(acc, lane);
+    int d = xidx<SPAN>(lane);
+    double dd = __longlong_as_double(0x7ff0000000000000ll);  // +inf: not admissible
+    if (admissible(i, b + d, wo.n_sub, excl)) {
+      if (wo.flat[oo + b + d]) {
+        dd = (double)m;  // reading 5: flat vs non-flat
+      } else {
+        // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i)
+        const double cov = acc[0] - wo.mu[oo + b + d] * asum;
+        dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + b + d]);
+      }
+    }
+#pragma unroll
+    for (int q = 16; q >= 1; q >>= 1) {  // warp argmin of (dd, d), smallest d on ties
+      const double od = __shfl_xor_sync(0xffffffffu, dd, q);
+      const int oi = __shfl_xor_sync(0xffffffffu, d, q);
+      if (od < dd || (od == dd && oi < d)) {
+        dd = od;
+        d = oi;
+      }
+    }
+    j = dd < __longlong_as_double(0x7ff0000000000000ll) ? b + d : -1;
+    // ---- its distance from the definition, by explicit differences ---------------------------
     if (j < 0) {
-      p = __longlong_as_double(0x7ff8000000000000ll);  // no candidate (band not covered)
+      p = __longlong_as_double(0x7ff8000000000000ll);
     } else if (wo.flat[oo + j]) {
       p = sqm;
     } else {
-      const T* R = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
-      const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
-      const double mi = w.mu[o + i], mj = wo.mu[oo + j];
+      const double mj = wo.mu[oo + j];
       // z = (x - mu) * (1/sigma): one division per row instead of per element (<= 1 ulp from
       // the textbook quotient; the oracle divides)
       const double ii = 1.0 / w.sig64[o + i], ij = 1.0 / wo.sig64[oo + j];
-      double acc = 0.0;
-#pragma unroll 4
-      for (int s = lane; s < m; s += 32) {
-        const double zi = __dmul_rn((double)R[i + s] - mi, ii);
-        const double zj = __dmul_rn((double)Ro[j + s] - mj, ij);
-        const double e = zi - zj;
-        acc = __dadd_rn(acc, __dmul_rn(e, e));
+      double acc2 = 0.0;
+      if (m <= MC) {  // the staged chunk still holds both windows (member d at offset d)
+        for (int s = lane; s < m; s += 32) {
+          const double zi = __dmul_rn(xi[s] - mi, ii);
+          const double zj = __dmul_rn(xo[s + d] - mj, ij);
+          const double e = zi - zj;
+          acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
+        }
+      } else {
+        for (int s = lane; s < m; s += 32) {
+          const double zi = __dmul_rn((double)R[i + s] - mi, ii);
+          const double zj = __dmul_rn((double)Ro[j + s] - mj, ij);
+          const double e = zi - zj;
+          acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
+        }
       }
 #pragma unroll
-      for (int q = 16; q > 0; q >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, q);
-      p = sqrt(acc);
+      for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+      p = sqrt(acc2);
     }
     if (nf > 0) {
       const int64_t f = smallest_adm_flat(F, nf, i, excl);
@@ -229,26 +253,27 @@ __global__ void finalize_kernel(MpDev w, MpDev wo, int excl, T* __restrict__ P, 
 }  // namespace
 
 cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* P, int64_t* I,
-                               cudaStream_t st) {
-  const int64_t threads = w.n_sub * 32;
-  dim3 grid((unsigned)((threads + 255) / 256), (unsigned)w.k);
+                               cudaStream_t st, int64_t row_lo, int64_t row_hi) {
+  if (row_hi < 0) row_hi = w.n_sub;
+  if (row_hi <= row_lo) return cudaSuccess;
+  dim3 grid((unsigned)((row_hi - row_lo + kFinWarps - 1) / kFinWarps), (unsigned)w.k);
+  const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
+#define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
   switch (w.span) {
     case 4:
-      if (f32) finalize_kernel<float, 4><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<float*>(P), I);
-      else finalize_kernel<double, 4><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<double*>(P), I);
+      if (f32) SKMP_FIN(float, 4); else SKMP_FIN(double, 4);
       break;
     case 8:
-      if (f32) finalize_kernel<float, 8><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<float*>(P), I);
-      else finalize_kernel<double, 8><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<double*>(P), I);
+      if (f32) SKMP_FIN(float, 8); else SKMP_FIN(double, 8);
       break;
     case 16:
-      if (f32) finalize_kernel<float, 16><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<float*>(P), I);
-      else finalize_kernel<double, 16><<<grid, 256, 0, st>>>(w, wo, excl, static_cast<double*>(P), I);
+      if (f32) SKMP_FIN(float, 16); else SKMP_FIN(double, 16);
       break;
     default:
       return cudaErrorInvalidValue;
   }
+#undef SKMP_FIN
   count_launches(1);
   return cudaGetLastError();
 }

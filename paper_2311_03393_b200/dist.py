@@ -18,8 +18,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (F32, F64, Sketch, detect_dimension, mp_band, mp_create, mp_finalize, mp_join, mp_keys,
-               sketch_refresh, sketch_view64)
+from . import (F32, F64, Sketch, detect_dimension, mp_band, mp_create, mp_finalize, mp_finalize_rows,
+               mp_join, mp_keys, sketch_refresh, sketch_view64)
 
 INT64_MIN = -(1 << 63)
 
@@ -83,9 +83,13 @@ def detect_dimension_dist(sk: Sketch, sources, t: int, g: int, m: int, device, g
     every rank scores its members of J_g (discord_dims), then the (score, plan order) maxima are
     all-gathered and every rank returns the same (id*, score, nn).  Ranks hold contiguous id
     shards, so (rank, local order) is the global plan order of Alg. 3's scan."""
+    return gather_dimension(detect_dimension(sk, sources, t, g, m), device, group)
+
+
+def gather_dimension(loc, device, group=None):
+    """All-gather every rank's local Alg. 3 winner (id, score, nn) or None and return the global
+    one: the first strict maximum in rank order (ranks hold contiguous id shards)."""
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    loc = detect_dimension(sk, sources, t, g, m)
     row = torch.tensor([-1.0, 0.0, 0.0, 0.0], dtype=torch.float64, device=device) if loc is None else \
         torch.tensor([1.0, loc[1], float(loc[0]), float(loc[2])], dtype=torch.float64, device=device)
     allr = [torch.empty_like(row) for _ in range(world)]
@@ -96,4 +100,23 @@ def detect_dimension_dist(sk: Sketch, sources, t: int, g: int, m: int, device, g
         if ok > 0 and (best is None or sc > best[1]):  # strict: the earliest rank wins ties
             best = (int(j), sc, int(nn))
     return best
+
+
+def row_range(n_sub: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous window slice of `rank` for the sharded finalize."""
+    b = np.linspace(0, n_sub, world + 1).astype(np.int64)
+    return int(b[rank]), int(b[rank + 1])
+
+
+def finalize_dist(w, group=None, dst: int = 0):
+    """Sharded finalize after the key reduce (every rank holds all keys): each rank resolves its
+    slice of windows into zero-filled full-size P / I, which are sum-reduced to rank `dst` (x + 0
+    is exact).  Returns (P, I, inert) on `dst`, None elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = row_range(w.n_sub, world, rank)
+    P, I, inert = mp_finalize_rows(w, lo, hi)
+    dist.reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
+    dist.reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
+    return (P, I, inert) if rank == dst else None
 

@@ -94,6 +94,20 @@ def _worker(rank, world, port, q):
         Rt = torch.from_numpy(Rp.copy())
         dist.all_reduce(Rt, op=dist.ReduceOp.SUM)
         out["sketch"] = Rt.numpy()
+        # ---- sharded finalize: zero-filled slices sum-reduce to the full profile -----------
+        P, I, _ = ref.selfjoin_brute(r, m, excl)
+        lo, hi = sdist.row_range(len(P), world, rank)
+        Ps = torch.zeros(len(P), dtype=torch.float64)
+        Is = torch.zeros(len(P), dtype=torch.int64)
+        Ps[lo:hi] = torch.from_numpy(P[lo:hi])
+        Is[lo:hi] = torch.from_numpy(I[lo:hi])
+        dist.reduce(Ps, 0, op=dist.ReduceOp.SUM)
+        dist.reduce(Is, 0, op=dist.ReduceOp.SUM)
+        out["fin"] = (Ps.numpy(), Is.numpy(), (lo, hi))
+        # ---- Alg. 3 across ranks: global first strict maximum in rank order --------------
+        locs = [(11, 2.5, 40), (23, 2.5, 7)]          # a tie: rank 0 must win
+        out["dim_tie"] = sdist.gather_dimension(locs[rank], "cpu")
+        out["dim_none"] = sdist.gather_dimension(None if rank == 0 else (5, 1.0, 3), "cpu")
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -129,6 +143,13 @@ def test_two_rank_bands_and_reductions():
                 if j[i] != I[i]:  # only a tie at the key's precision is acceptable
                     d = math.sqrt(((Z[i] - Z[j[i]]) ** 2).sum())
                     assert abs(d - P[i]) <= (1e-6 if words == 1 else 1e-12) * max(P[i], 1.0), (i, j[i], I[i])
+    # sharded finalize reassembles the whole profile on rank 0; ranks' slices tile [0, n_sub)
+    Pf, If, (lo0, hi0) = res[0]["fin"]
+    assert np.array_equal(Pf, P) and np.array_equal(If, I)
+    assert lo0 == 0 and res[0]["fin"][2][1] == res[1]["fin"][2][0] and res[1]["fin"][2][1] == len(P)
+    for rank in range(world):
+        assert res[rank]["dim_tie"] == (11, 2.5, 40)
+        assert res[rank]["dim_none"] == (5, 1.0, 3)
     cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=600, k=3)
     T = synthgen.streams(cfg)
     g, s = plan_count_sketch(np.arange(cfg.d), cfg.k, cfg.seed)
