@@ -83,7 +83,7 @@ def workload_desc(cfg, top):
     return (f"{cfg.name}: d={cfg.d} streams, n={cfg.n}, m={cfg.m}, k={cfg.k}, {cfg.dtype}, "
             f"{'count sketch' if cfg.proj == 'count' else 'dense projection'}, {cfg.kind}; step = "
             f"sketch_build + add {cfg.extra.get('n_add', 0)} + delete {cfg.extra.get('n_del', 0)} + "
-            f"self-join + top-{top}")
+            f"self-join + top-{top} + Alg. 3 dimension of the top discord")
 
 
 # ----------------------------------------------------------------------------------------------
@@ -351,8 +351,20 @@ def main():
             host_del = Tdel.cpu().pin_memory() if Tdel is not None else None
         except RuntimeError as ex:
             log(f"[rank {rank}] e2e skipped: {ex}")
+    dim_rows = None
     if not args.no_e2e and host_T is not None:
         step(host_T, host_add, host_del)  # warm the staging pool
+        # members of the top discord's group (the streams Alg. 3 stages each step), all ranks
+        gsk = skmp.sketch_build(Td, my_ids, k, seed=cfg.seed)
+        if Tadd is not None:
+            skmp.sketch_add_dim(gsk, Tadd, my_add)
+        if Tdel is not None:
+            skmp.sketch_del_dim(gsk, Tdel, my_del)
+        gt = torch.tensor([res[0][0].g if rank == 0 else 0], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.broadcast(gt, 0)
+        dim_rows = len(skmp.group_rows(gsk, int(gt.item())))
+        gsk.free()
         barrier()
         s0, s1 = ev(), ev()
         s0.record()
@@ -367,6 +379,7 @@ def main():
         esz = host_T.element_size()
         h2d = (host_T.numel() + (0 if host_add is None else host_add.numel())
                + (0 if host_del is None else host_del.numel())) * esz
+        h2d += dim_rows * cfg.n * esz  # Alg. 3 stages its group's host rows
         if world > 1:
             hb = torch.tensor([h2d], device=dev, dtype=torch.float64)
             dist.all_reduce(hb)

@@ -248,7 +248,8 @@ skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, 
  * P:L129-133, evaluated by explicit differences in FP64; flat windows per reading 5 relative
  * to max|T_j|; smallest t on ties), and j* = the FIRST strict maximiser in the listed order
  * (Alg. 3 lines 3-7, reading 20).  The refinement join of P:L303-304 is mp_selfjoin on row j*.
- *   T       [dev|host] (max(rows)+1) x ld streams (dtype), n samples each.
+ *   T       [dev|host] (max(rows)+1) x ld streams (dtype), n samples each (a host matrix is
+ *           staged row by row: only the listed rows cross PCIe).
  *   rows    [host] nrows stream rows of T (the members of J_{g*}, in group order).
  *   t_star  the discord time from discord_topk, 0 <= t_star < n - m + 1.
  *   excl    exclusion radius; < 0 -> ceil(m/2) (reading 7).

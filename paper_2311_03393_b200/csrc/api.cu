@@ -889,8 +889,23 @@ skmp_status discord_dims(const void* T, int64_t ld, int64_t n, int32_t dtype, co
   Temps tmp(st);
   const void* Tdev;
   int64_t ldd;
-  if ((s = stage_input(T, maxrow + 1, n, ld, dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
   std::vector<int64_t> hrows(rows, rows + nrows);
+  if (is_device_ptr(T)) {
+    Tdev = T;
+    ldd = ld;
+  } else {  // host streams: stage only the listed rows (compacted), not the whole matrix
+    const size_t es = elem_size(dtype);
+    char* d = nullptr;
+    SKMP_CUDA(tmp.alloc(&d, (size_t)nrows * (size_t)n * es));
+    for (int64_t q = 0; q < nrows; ++q) {
+      SKMP_CUDA(cudaMemcpyAsync(d + (size_t)q * n * es, static_cast<const char*>(T) + (size_t)rows[q] * ld * es,
+                                (size_t)n * es, cudaMemcpyHostToDevice, st));
+      hrows[(size_t)q] = q;
+    }
+    Tdev = d;
+    ldd = n;
+  }
+  (void)maxrow;
   int64_t* d_rows;
   if ((s = upload(hrows, &d_rows, tmp)) != SKMP_OK) return s;
   double* d_score;

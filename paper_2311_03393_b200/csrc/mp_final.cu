@@ -104,21 +104,17 @@ __device__ __forceinline__ void fin_stage(double* xi, double* xo, const T* R, co
   constexpr int MC = FinChunk<T>::MC;
   constexpr int NI = MC / 32, NO = (MC + SPAN - 1 + 31) / 32;
   T vi[NI], vo[NO];
-  const T* ri = R + i + s0 + lane;
 #pragma unroll
-  for (int q = 0; q < NI; ++q) vi[q] = (lane + 32 * q < len) ? ri[32 * q] : (T)0;
-  if (len == MC && b + s0 >= 0 && b + s0 + MC + SPAN - 1 <= n_o) {  // interior: no clamping
-    const T* ro = Ro + b + s0 + lane;
+  for (int q = 0; q < NI; ++q) {
+    const int s = lane + 32 * q;
+    vi[q] = s < len ? R[i + s0 + s] : (T)0;
+  }
 #pragma unroll
-    for (int q = 0; q < NO; ++q) vo[q] = (lane + 32 * q < MC + SPAN - 1) ? ro[32 * q] : (T)0;
-  } else {
-#pragma unroll
-    for (int q = 0; q < NO; ++q) {
-      const int t = lane + 32 * q;
-      int64_t idx = b + s0 + t;
-      idx = idx < 0 ? 0 : (idx >= n_o ? n_o - 1 : idx);  // only inadmissible members read clamped data
-      vo[q] = t < len + SPAN - 1 ? Ro[idx] : (T)0;
-    }
+  for (int q = 0; q < NO; ++q) {
+    const int t = lane + 32 * q;
+    int64_t idx = b + s0 + t;
+    idx = idx < 0 ? 0 : (idx >= n_o ? n_o - 1 : idx);  // only inadmissible members read clamped data
+    vo[q] = t < len + SPAN - 1 ? Ro[idx] : (T)0;
   }
 #pragma unroll
   for (int q = 0; q < NI; ++q) xi[lane + 32 * q] = (double)vi[q];

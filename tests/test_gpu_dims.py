@@ -135,3 +135,32 @@ def test_alg2_alg3_refine_end_to_end_c2(cuda):
     assert int(torch.argmax(Pj[0])) == t_r
     print(f"C2: Alg. 2 (t*={top.t}, g*={top.g}), Alg. 3 j*={jstar} (score {sc[js]:.4f}), "
           f"refined discord t={t_r} score {s_r:.4f}")
+
+
+def test_detect_dimension_after_add_delete(cuda):
+    """Alg. 3 over a group whose members come from two device matrices (original streams with
+    some deleted, plus added streams), as bench.py calls it, against the oracle on the final
+    member set in plan order."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.scaled(synthgen.CONFIGS["c4"], d=60, n=3000, k=4, m=64)
+    ids = np.arange(60, dtype=np.uint64)
+    add = np.arange(60, 72, dtype=np.uint64)
+    dele = np.array([3, 7, 22, 41], dtype=np.uint64)
+    T = synthgen.streams(cfg, ids)
+    Ta = synthgen.streams(cfg, add)
+    Td = torch.from_numpy(T).to(cuda, torch.float64)
+    Tad = torch.from_numpy(Ta).to(cuda, torch.float64)
+    sk = skmp.sketch_build(Td, ids, cfg.k, seed=cfg.seed)
+    skmp.sketch_add_dim(sk, Tad, add)
+    skmp.sketch_del_dim(sk, Td[dele.astype(np.int64)].contiguous(), dele)
+    t_star, g = 1234, 2
+    got = skmp.detect_dimension(sk, [(Td, ids), (Tad, add)], t_star, g, cfg.m)
+    plan = skmp.sketch_plan(sk)
+    members = [int(j) for j, gg in zip(plan["ids"], plan["groups"]) if gg == g]
+    allT = {int(j): T[q] for q, j in enumerate(ids)}
+    allT.update({int(j): Ta[q] for q, j in enumerate(add)})
+    M = np.stack([allT[j] for j in members])
+    sc, nn, js = ref.dimension_detection(M, list(range(len(members))), t_star, cfg.m)
+    assert got[0] == members[js] and abs(got[1] - sc[js]) <= 1e-9 * sc[js] and got[2] == nn[js]
+    assert all(j not in members for j in dele.tolist())

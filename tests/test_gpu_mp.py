@@ -122,3 +122,28 @@ def test_mp_errors(cuda):
     with pytest.raises(skmp.SkmpError) as e:
         skmp.mp_selfjoin(R, 1)
     assert e.value.name == "SKMP_E_INVALID_ARG"
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mp_finalize_rows_slices(cuda, dtype):
+    """mp_finalize_rows over disjoint window slices (the multi-GPU sharded finalize) reproduces
+    mp_finalize exactly."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    X = synthgen.mp_series(3, 3000, seed=71, kind="mix")
+    R = torch.from_numpy(X).to(cuda, torch.float32 if dtype == "f32" else torch.float64)
+    w = skmp.mp_create(R, 40, reseed_rows=256)
+    skmp.mp_join(w)
+    P, I, inert = skmp.mp_finalize(w)
+    n_sub = 3000 - 40 + 1
+    Ps = torch.zeros_like(P)
+    Is = torch.zeros_like(I)
+    for lo, hi in ((0, 1), (1, 777), (777, 778), (778, n_sub)):
+        Pp, Ip, _ = skmp.mp_finalize_rows(w, lo, hi)
+        Ps += Pp
+        Is += Ip
+    torch.cuda.synchronize()
+    assert torch.equal(Ps, P) and torch.equal(Is, I)
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_finalize_rows(w, 5, n_sub + 1)
+    w.free()
