@@ -110,9 +110,12 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-__device__ __forceinline__ double max3(double a, double b, double c) { return fmax(a, fmax(b, c)); }
+// FP64 maxima as plain compare-select: fmax's NaN quieting costs two extra instructions per
+// merge and the join's values are never NaN (finite rho or the -inf of a masked cell)
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double max3(double a, double b, double c) { return dmax(a, dmax(b, c)); }
 __device__ __forceinline__ float max2(float a, float b) { return fmaxf(a, b); }
-__device__ __forceinline__ double max2(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ double max2(double a, double b) { return dmax(a, b); }
 
 // max of n values with 3-input FMNMX3 where possible: ceil((n-1)/2) operations
 template <typename T, int N>
