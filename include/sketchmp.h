@@ -117,6 +117,17 @@ skmp_status sketch_add_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld
 skmp_status sketch_del_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld,
                            const uint64_t* ids, void* stream);
 
+/* Point updates (§3.3: "if only the i-th time point of the j-th dimension is
+ * updated, to increase its value by delta, then R^(g)_i = R^(g)_i + s(j) delta"): for q < count,
+ * stream ids[q] moves by delta[q] at time t[q].  Reading 24: delta is in the stream's own units
+ * and the sketch keeps the stream z-normalised with its STORED statistics, so the sketch moves by
+ * s(j) delta / sigma_j (DENSE: S_gj delta / sigma_j in every group); the statistics are not
+ * re-estimated.  FP64 atomics on the master sketch (repeated (id, t) pairs accumulate), then the
+ * touched entries are re-rounded to dtype.  ids/t/delta [host] count.  Asynchronous.
+ * Errors: INVALID_ARG (NULL, count < 0, t outside [0, n)), UNKNOWN_DIM, CUDA, OOM. */
+skmp_status sketch_point_update(skmp_sketch* h, const uint64_t* ids, const int64_t* t, const double* delta,
+                                int64_t count, void* stream);
+
 /* Borrowed views (valid until the next add/del/free).  R: [dev] k x n, ld = n, dtype.
  * R64: [dev] k x n FP64 master accumulators. */
 skmp_status sketch_view(const skmp_sketch* h, const void** R, int32_t* k, int64_t* n, int64_t* d,

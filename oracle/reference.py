@@ -18,6 +18,8 @@ Function pins (tests/test_oracle_pins.py):
   detect (identity plan)     -> per-stream exact profiles of Def. 5
   dimension_detection        -> scipy cdist distance profile; exact repeat (periodic stream)
                                 -> score 0; planted single-stream burst -> j* on it
+  sketch(stats=...)          -> own statistics reproduce sketch(); a point change of one sample
+                                moves one sketch entry by s(j) delta / sigma_j (closed form)
   abjoin_brute               -> scipy cdist between the two window sets (rows and columns);
                                 a window copied into the other series -> 0 at its copy
 """
@@ -69,14 +71,15 @@ def znormalize(x: np.ndarray) -> np.ndarray:
 # a3/a4: Alg. 1: R^(g) = sum_{j in J_g} s(j) T_bar^(j), J_g = {j : h(j) = g}
 # ------------------------------------------------------------------------------------------
 
-def sketch(T: np.ndarray, k: int, groups=None, signs=None, S: np.ndarray | None = None):
+def sketch(T: np.ndarray, k: int, groups=None, signs=None, S: np.ndarray | None = None, stats=None):
     """Returns (R (k x n, FP64), mu, sigma).  Count sketch when `groups`/`signs` are given
     (one entry per row of T, in input order); dense projection R = S T_bar when S (k x d) is
     given (reading 1).  Sums run sequentially over j in ascending input order, exactly as the
-    loop of Alg. 1 lines 3-5."""
+    loop of Alg. 1 lines 3-5.  `stats` = (mu, sigma) z-normalises with given (stored)
+    statistics instead of the data's own (§3.3 point updates, reading 24)."""
     T = np.asarray(T, dtype=np.float64)
     d, n = T.shape
-    mu, sigma = stream_stats(T)
+    mu, sigma = stream_stats(T) if stats is None else (np.asarray(stats[0], float), np.asarray(stats[1], float))
     R = np.zeros((k, n))
     for j in range(d):                      # Alg. 1 line 3: for j in [0, ..., d-1]
         z = (T[j] - mu[j]) / sigma[j]       # T_bar^(j)

@@ -3,7 +3,8 @@
 Argument marshalling only: every step of the path runs in libsketchmp.so's CUDA kernels.
 PyTorch supplies device memory and the current CUDA stream.  The same names as the C-ABI:
 
-    sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_view, sketch_view64,
+    sketch_hash_plan, sketch_build, sketch_add_dim, sketch_del_dim, sketch_point_update, sketch_view,
+    sketch_view64,
     sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize,
     mp_finalize_rows, mp_free,
     mp_selfjoin, mp_abjoin, discord_topk, discord_dims
@@ -72,6 +73,7 @@ _SIGS = {
     "sketch_view": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I32), ctypes.POINTER(_I64),
                                    ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
     "sketch_view64": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "sketch_point_update": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P]),
     "sketch_plan": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "sketch_free": (None, [_P]),
     "mp_create": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, ctypes.POINTER(_P)]),
@@ -249,6 +251,15 @@ def sketch_del_dim(sk: Sketch, T, ids, stream=None):
     ids = np.ascontiguousarray(ids, dtype=np.uint64)
     ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
     _check(lib().sketch_del_dim(sk.handle, _ptr(T), T.shape[0], ld, _ptr(ids), _stream(stream)))
+
+
+def sketch_point_update(sk: Sketch, ids, t, delta, stream=None):
+    """§3.3 point updates: stream ids[q] changes by delta[q] at time t[q] (its own units)."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    t = np.ascontiguousarray(t, dtype=np.int64)
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    assert len(ids) == len(t) == len(delta)
+    _check(lib().sketch_point_update(sk.handle, _ptr(ids), _ptr(t), _ptr(delta), len(ids), _stream(stream)))
 
 
 def sketch_view(sk: Sketch):

@@ -467,6 +467,48 @@ skmp_status sketch_del_dim(skmp_sketch* h, const void* T, int64_t nb, int64_t ld
   return ok();
 }
 
+skmp_status sketch_point_update(skmp_sketch* h, const uint64_t* ids, const int64_t* t, const double* delta,
+                                int64_t count, void* stream) {
+  if (!h || (count > 0 && (!ids || !t || !delta)) || count < 0)
+    return set_error(SKMP_E_INVALID_ARG, "sketch_point_update: NULL argument or count < 0");
+  std::vector<int64_t> idx;
+  std::vector<double> coef, dl;
+  const bool dense = h->proj == SKMP_PROJ_DENSE;
+  idx.reserve((size_t)count * (dense ? h->k : 1));
+  for (int64_t q = 0; q < count; ++q) {
+    auto it = h->pos.find(ids[q]);
+    if (it == h->pos.end()) return set_error(SKMP_E_UNKNOWN_DIM, "sketch_point_update: stream id not in the sketch", q);
+    if (t[q] < 0 || t[q] >= h->n) return set_error(SKMP_E_INVALID_ARG, "sketch_point_update: time outside [0, n)", q);
+    const size_t a = (size_t)it->second;
+    // reading 24: the stream's value moves by delta in its own units; the sketch holds the stream
+    // z-normalised with its STORED statistics, so its contribution moves by delta / sigma_j
+    if (dense) {
+      for (int g = 0; g < h->k; ++g) {
+        idx.push_back((int64_t)g * h->n + t[q]);
+        coef.push_back(h->Scol[a * (size_t)h->k + (size_t)g] / h->sigma[a]);
+        dl.push_back(delta[q]);
+      }
+    } else {
+      idx.push_back((int64_t)h->g[a] * h->n + t[q]);
+      coef.push_back((double)h->s[a] / h->sigma[a]);
+      dl.push_back(delta[q]);
+    }
+  }
+  if (count == 0) return ok();
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  int64_t* d_idx;
+  double *d_coef, *d_delta;
+  if ((s = upload(idx, &d_idx, tmp)) != SKMP_OK) return s;
+  if ((s = upload(coef, &d_coef, tmp)) != SKMP_OK) return s;
+  if ((s = upload(dl, &d_delta, tmp)) != SKMP_OK) return s;
+  SKMP_CUDA(launch_point_update(h->R64, h->R, h->dtype, d_idx, d_coef, d_delta, (int64_t)idx.size(), st));
+  h->st = st;
+  return ok();
+}
+
 skmp_status sketch_view(const skmp_sketch* h, const void** R, int32_t* k, int64_t* n, int64_t* d,
                         int32_t* dtype) {
   if (!h) return set_error(SKMP_E_INVALID_ARG, "sketch_view: NULL handle");

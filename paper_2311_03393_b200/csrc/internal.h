@@ -159,6 +159,10 @@ cudaError_t launch_dims(const void* X, int64_t ld, int64_t n, int dtype, const i
 // kernel-launch accounting (skmp_launch_count): every launcher reports its launches
 void count_launches(int64_t n);
 
+// §3.3 point updates: R64[idx[q]] += coef[q] * delta[q], then R[idx] = dtype(R64[idx]) (all [dev])
+cudaError_t launch_point_update(double* R64, void* R, int dtype, const int64_t* idx, const double* coef,
+                                const double* delta, int64_t count, cudaStream_t st);
+
 // R = dtype(R64) (sketch_refresh)
 cudaError_t launch_cast_r(const double* R64, void* R, int64_t count, int dtype, cudaStream_t st);
 

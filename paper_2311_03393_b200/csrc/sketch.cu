@@ -317,6 +317,20 @@ __global__ void project_dense_kernel(const T* __restrict__ Tm, int64_t ld, int64
   }
 }
 
+// §3.3 point updates: R64[idx[q]] += coef[q] * delta[q] (FP64 atomics: several updates may hit
+// one entry), then the touched entries are re-rounded to the dtype copy.
+__global__ void point_add_kernel(double* __restrict__ R64, const int64_t* __restrict__ idx,
+                                 const double* __restrict__ coef, const double* __restrict__ delta,
+                                 int64_t count) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < count) atomicAdd(R64 + idx[q], __dmul_rn(coef[q], delta[q]));
+}
+__global__ void point_cast_kernel(const double* __restrict__ R64, float* __restrict__ R,
+                                  const int64_t* __restrict__ idx, int64_t count) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < count) R[idx[q]] = (float)R64[idx[q]];
+}
+
 __global__ void cast_kernel(const double* __restrict__ a, float* __restrict__ b, int64_t count) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -330,6 +344,19 @@ cudaError_t launch_cast_r(const double* R64, void* R, int64_t count, int dtype, 
   const int64_t blocks = (count + 255) / 256;
   cast_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, st>>>(R64, static_cast<float*>(R), count);
   count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_point_update(double* R64, void* R, int dtype, const int64_t* idx, const double* coef,
+                                const double* delta, int64_t count, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((count + 255) / 256);
+  point_add_kernel<<<blocks, 256, 0, st>>>(R64, idx, coef, delta, count);
+  count_launches(1);
+  if (dtype == SKMP_F32) {
+    point_cast_kernel<<<blocks, 256, 0, st>>>(R64, static_cast<float*>(R), idx, count);
+    count_launches(1);
+  }
   return cudaGetLastError();
 }
 

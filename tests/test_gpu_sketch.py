@@ -177,3 +177,46 @@ def test_sketch_errors(cuda):
     with pytest.raises(skmp.SkmpError) as e:
         skmp.sketch_del_dim(sk, T[:1], np.array([9]))
     assert e.value.name == "SKMP_E_UNKNOWN_DIM"
+
+
+@pytest.mark.parametrize("dtype,proj", [("f64", "count"), ("f32", "count"), ("f64", "dense")])
+def test_point_updates(cuda, dtype, proj):
+    """§3.3 point updates (reading 24) vs the oracle's Alg. 1 on the modified data
+    with the stored statistics; repeated (id, t) pairs accumulate."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=30, n=3000, k=5)
+    T = synthgen.streams(cfg)
+    ids = np.arange(100, 130, dtype=np.uint64)          # ids need not equal rows
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    Td = torch.from_numpy(T).to(cuda, tdt)
+    To = Td.double().cpu().numpy()
+    S = np.random.default_rng(5).standard_normal((cfg.k, cfg.d)) if proj == "dense" else None
+    if proj == "dense":
+        sk = skmp.sketch_build(Td, ids, cfg.k, proj=skmp.PROJ_DENSE, S=S)
+    else:
+        sk = skmp.sketch_build(Td, ids, cfg.k, seed=cfg.seed)
+    rng = np.random.default_rng(9)
+    rows = rng.integers(0, cfg.d, 400)
+    ts = rng.integers(0, cfg.n, 400)
+    rows[-5:], ts[-5:] = rows[0], ts[0]                  # repeats of one (id, t)
+    dl = rng.standard_normal(400) * 3.0
+    skmp.sketch_point_update(sk, ids[rows], ts, dl)
+    torch.cuda.synchronize()
+    T2 = To.copy()
+    np.add.at(T2, (rows, ts), dl)
+    plan = skmp.sketch_plan(sk)
+    if proj == "dense":
+        R_or, _, _ = ref.sketch(T2, cfg.k, S=S, stats=(plan["mu"], plan["sigma"]))
+        bound = _terms_bound(T2, plan["mu"], plan["sigma"], None, None, cfg.k, S=S)
+    else:
+        g, s = plan_count_sketch(ids, cfg.k, cfg.seed)
+        R_or, _, _ = ref.sketch(T2, cfg.k, g, s, stats=(plan["mu"], plan["sigma"]))
+        bound = _terms_bound(T2, plan["mu"], plan["sigma"], g, s, cfg.k)
+    _check_R(sk.R64.cpu().numpy(), sk.R.cpu().numpy(), R_or, bound, dtype)
+    with pytest.raises(skmp.SkmpError) as e:
+        skmp.sketch_point_update(sk, [999], [0], [1.0])
+    assert e.value.name == "SKMP_E_UNKNOWN_DIM"
+    with pytest.raises(skmp.SkmpError) as e:
+        skmp.sketch_point_update(sk, [ids[0]], [cfg.n], [1.0])
+    assert e.value.name == "SKMP_E_INVALID_ARG"

@@ -343,3 +343,30 @@ def test_abjoin_brute_vs_cdist_and_planted(seed):
     Pt, It = ref.abjoin_brute(b, a, m)
     np.testing.assert_allclose(Pt, D.min(axis=0), rtol=1e-12, atol=1e-12)
     assert P[t] < 1e-6 and Pt[u] < 1e-6
+
+
+def test_sketch_with_stored_stats_point_update_closed_form():
+    """§3.3 point update under reading 24: the plain Alg. 1 loop on the modified data
+    with the STORED statistics moves exactly one entry per update by s(j) delta / sigma_j (dense:
+    S_gj delta / sigma_j in every group); with the data's own statistics it equals sketch()."""
+    cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=400, k=3)
+    T = synthgen.streams(cfg)
+    g, s = plan_count_sketch(np.arange(cfg.d), cfg.k, cfg.seed)
+    R, mu, sig = ref.sketch(T, cfg.k, g, s)
+    R2, _, _ = ref.sketch(T, cfg.k, g, s, stats=(mu, sig))
+    np.testing.assert_array_equal(R, R2)
+    T2 = T.copy()
+    T2[4, 123] += 2.5
+    T2[7, 5] -= 1.25
+    Ru, _, _ = ref.sketch(T2, cfg.k, g, s, stats=(mu, sig))
+    want = R.copy()
+    want[g[4], 123] += s[4] * 2.5 / sig[4]
+    want[g[7], 5] += s[7] * -1.25 / sig[7]
+    np.testing.assert_allclose(Ru, want, rtol=0, atol=1e-12 * np.abs(R).max())
+    S = np.random.default_rng(3).standard_normal((cfg.k, cfg.d))
+    Rd, mu_d, sig_d = ref.sketch(T, cfg.k, S=S)
+    Rdu, _, _ = ref.sketch(T2, cfg.k, S=S, stats=(mu_d, sig_d))
+    want = Rd.copy()
+    want[:, 123] += S[:, 4] * 2.5 / sig_d[4]
+    want[:, 5] += S[:, 7] * -1.25 / sig_d[7]
+    np.testing.assert_allclose(Rdu, want, rtol=0, atol=1e-12 * np.abs(Rd).max())
