@@ -696,7 +696,7 @@ skmp_status join_band(const MpDev& wr, const MpDev& wc, int64_t lo, int64_t hi, 
     prefix[(size_t)b + 1] = prefix[(size_t)b] + (rows > 0 ? (rows + wr.L - 1) / wr.L : 0);
   }
   const int64_t ntiles = prefix[(size_t)nblk];
-  if (ntiles > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "mp_join: too many tiles; raise reseed_rows");
+  if (ntiles * wr.k > INT32_MAX) return set_error(SKMP_E_INVALID_ARG, "mp_join: too many tiles; raise reseed_rows");
   Temps tmp(st);
   int64_t* d_prefix = nullptr;
   skmp_status s = upload(prefix, &d_prefix, tmp);

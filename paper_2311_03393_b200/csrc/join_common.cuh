@@ -58,6 +58,7 @@ struct JoinArgs {
   const int64_t* prefix;  // nblk + 1 cumulative tile counts
   int64_t nblk;
   int64_t blk0;
+  int k;                  // series (the grid enumerates tiles of all series, block-major)
 };
 
 inline JoinArgs make_join_args(const MpDev& wr, const MpDev& wc, int64_t dlo, int64_t dhi,
@@ -86,6 +87,7 @@ inline JoinArgs make_join_args(const MpDev& wr, const MpDev& wc, int64_t dlo, in
   a.prefix = prefix;
   a.nblk = nblk;
   a.blk0 = blk0;
+  a.k = wr.k;
   return a;
 }
 
@@ -208,17 +210,23 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 
-// tile of the band this CTA owns: binary search of the per-block tile prefix
-__device__ __forceinline__ void decode_tile(const JoinArgs& a, int64_t W, int64_t* delta0,
+// Tile of the band this CTA owns.  Launch order is diagonal-block-major across ALL series
+// (block b's tiles of series 0, 1, ..., k-1, then block b+1 ...): the nearest diagonals of every
+// series run first, so the profile thresholds are good early and later tiles publish rarely.
+// Global tile T lies in block b with prefix[b] k <= T < prefix[b+1] k (binary search).
+__device__ __forceinline__ void decode_tile(const JoinArgs& a, int64_t W, int k, int* g, int64_t* delta0,
                                             int64_t* i0, int64_t* i1) {
   const int64_t tile = blockIdx.x;
   int64_t lo = 0, hi = a.nblk - 1;
   while (lo < hi) {
     const int64_t mid = (lo + hi + 1) >> 1;
-    if (a.prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+    if (a.prefix[mid] * k <= tile) lo = mid; else hi = mid - 1;
   }
   const int64_t b = lo;
-  const int64_t rt = tile - a.prefix[b];
+  const int64_t nb = a.prefix[b + 1] - a.prefix[b];  // row tiles of block b (per series)
+  const int64_t local = tile - a.prefix[b] * k;
+  *g = (int)(local / nb);
+  const int64_t rt = local - (int64_t)(*g) * nb;
   *delta0 = (a.blk0 + b) * W;
   const int64_t dmin = *delta0 > a.dlo ? *delta0 : a.dlo;
   const int64_t rows = tile_rows(a.n_sub, a.n_sub_c, dmin);

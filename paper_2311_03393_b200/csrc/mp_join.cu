@@ -328,27 +328,10 @@ join_kernel(JoinArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = NT * D;
   __shared__ int64_t s_tile[3];
-  const int g = blockIdx.y;
-  if (threadIdx.x == 0) {
-    // binary search: block b with prefix[b] <= tile < prefix[b+1]
-    const int64_t tile = blockIdx.x;
-    int64_t lo = 0, hi = a.nblk - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (a.prefix[mid] <= tile) lo = mid; else hi = mid - 1;
-    }
-    const int64_t b = lo;
-    const int64_t rt = tile - a.prefix[b];
-    const int64_t delta0 = (a.blk0 + b) * W;
-    const int64_t dmin = delta0 > a.dlo ? delta0 : a.dlo;
-    const int64_t rows = tile_rows(a.n_sub, a.n_sub_c, dmin);
-    const int64_t i0 = rt * a.L;
-    const int64_t i1 = (i0 + a.L < rows) ? i0 + a.L : rows;
-    s_tile[0] = delta0;
-    s_tile[1] = i0;
-    s_tile[2] = i1;
-  }
+  __shared__ int s_g;
+  if (threadIdx.x == 0) decode_tile(a, W, a.k, &s_g, &s_tile[0], &s_tile[1], &s_tile[2]);
   __syncthreads();
+  const int g = s_g;
   const int64_t delta0 = s_tile[0], i0 = s_tile[1], i1 = s_tile[2];
   // rows are processed in whole D-row rotations; rows beyond the edges are masked cells
   const int64_t i1r = i0 + (((i1 - i0) + D - 1) / D) * D;
@@ -365,8 +348,7 @@ cudaError_t launch_join_t(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t 
   cudaError_t e = cudaFuncSetAttribute(join_kernel<T, D, NT, C>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
-  dim3 grid((unsigned)ntiles, (unsigned)w.k);
-  join_kernel<T, D, NT, C><<<grid, NT, smem, st>>>(a);
+  join_kernel<T, D, NT, C><<<(unsigned)(ntiles * w.k), NT, smem, st>>>(a);
   count_launches(1);
   return cudaGetLastError();
 }

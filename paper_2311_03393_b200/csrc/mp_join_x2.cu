@@ -299,9 +299,10 @@ __global__ void __launch_bounds__(NT, SKMP_X2_MINB)
 join_x2_kernel(JoinArgs a) {
   __shared__ Smem sm;
   __shared__ int64_t s_tile[3];
-  const int g = blockIdx.y;
-  if (threadIdx.x == 0) decode_tile(a, W, &s_tile[0], &s_tile[1], &s_tile[2]);
+  __shared__ int s_g;
+  if (threadIdx.x == 0) decode_tile(a, W, a.k, &s_g, &s_tile[0], &s_tile[1], &s_tile[2]);
   __syncwarp();
+  const int g = s_g;
   const int64_t delta0 = s_tile[0], i0 = s_tile[1];
   const int64_t i1 = i0 + ((s_tile[2] - i0 + DG - 1) / DG) * DG;  // whole rotations; tail masked
   const int tid = threadIdx.x;
@@ -433,8 +434,7 @@ cudaError_t launch_mp_join_x2(const MpDev& w, const MpDev& wc, int64_t dlo, int6
                               const int64_t* prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
                               cudaStream_t st) {
   const JoinArgs a = make_join_args(w, wc, dlo, dhi, prefix, nblk, blk0);
-  dim3 grid((unsigned)ntiles, (unsigned)w.k);
-  join_x2_kernel<<<grid, NT, 0, st>>>(a);
+  join_x2_kernel<<<(unsigned)(ntiles * w.k), NT, 0, st>>>(a);
   count_launches(1);
   return cudaGetLastError();
 }
