@@ -159,7 +159,7 @@ void sketch_free(skmp_sketch* h);
 typedef struct {
   int32_t m;            /* subsequence length, >= 2                                          */
   int32_t excl;         /* exclusion radius; < 0 -> ceil(m/2)                                 */
-  int32_t reseed_rows;  /* 0 -> default (FP32 8192, FP64 2048); rounded up to 64              */
+  int32_t reseed_rows;  /* 0 -> default (FP32 16384, FP64 2048); rounded up to 64             */
   int32_t reserved;     /* must be 0                                                          */
 } skmp_mp_cfg;
 

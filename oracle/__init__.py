@@ -17,5 +17,5 @@ invariant, brute force on tiny inputs, or a worked value; see DESIGN.md §4 for 
 from .hashplan import splitmix64_stream, cw_params, plan_count_sketch  # noqa: F401
 from .reference import (  # noqa: F401
     OracleError, stream_stats, znormalize, sketch, window_stats, znorm_windows, dist,
-    selfjoin_brute, selfjoin_rows, combine, topk_greedy, detect, dimension_detection, refine, abjoin_brute,
+    selfjoin_brute, selfjoin_rows, selfjoin_tierb, combine, topk_greedy, detect, dimension_detection, refine, abjoin_brute,
 )

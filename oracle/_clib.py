@@ -10,14 +10,15 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mp_brute.c")
+_SRCS = [_SRC, os.path.join(_HERE, "mp_tierb.c")]
 _LIB = os.path.join(_HERE, "libmpbrute.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -31,6 +32,10 @@ def _get():
         lib.oracle_mp_rows.argtypes = [
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
             ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_tierb_selfjoin.restype = ctypes.c_int
+        lib.oracle_tierb_selfjoin.argtypes = [
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_int]
         lib.oracle_window_stats.restype = None
         lib.oracle_window_stats.argtypes = [
             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
@@ -62,3 +67,18 @@ def window_stats(r: np.ndarray, m: int):
     flat = np.empty(n_sub, dtype=np.uint8)
     lib.oracle_window_stats(r.ctypes.data, r.shape[0], m, mu.ctypes.data, sig.ctypes.data, flat.ctypes.data)
     return mu, sig, flat.astype(bool)
+
+
+def tierb_selfjoin(r: np.ndarray, m: int, excl: int, reseed: int = 65536, threads: int = 0):
+    lib = _get()
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    n_sub = r.shape[0] - m + 1
+    P = np.empty(n_sub)
+    I = np.empty(n_sub, dtype=np.int64)
+    rc = lib.oracle_tierb_selfjoin(r.ctypes.data, r.shape[0], m, excl, reseed, P.ctypes.data, I.ctypes.data,
+                                   int(threads))
+    if rc != 0:
+        from .reference import OracleError
+        raise OracleError({-1: "no_admissible", -2: "flat_windows_unsupported"}.get(rc, "oom"))
+    return P, I
+

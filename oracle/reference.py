@@ -14,6 +14,7 @@ Function pins (tests/test_oracle_pins.py):
   selfjoin_brute             -> scipy.spatial.distance.cdist on the same z-windows;
                                 planted motif -> 0; bounds 0 <= P <= 2 sqrt(m)
   selfjoin_rows (C)          -> selfjoin_brute on tiny inputs
+  selfjoin_tierb (C, tier B) -> selfjoin_brute to 1e-10 relative (incl. re-seed boundaries)
   combine / topk_greedy      -> an independent sort-then-scan reimplementation
   detect (identity plan)     -> per-stream exact profiles of Def. 5
   dimension_detection        -> scipy cdist distance profile; exact repeat (periodic stream)
@@ -177,6 +178,16 @@ def selfjoin_rows(r: np.ndarray, m: int, excl: int | None = None, rows=None, thr
         raise OracleError("no_admissible", n_sub)
     rows = np.arange(n_sub, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
     return mp_rows(r, m, excl, rows, threads)
+
+
+def selfjoin_tierb(r: np.ndarray, m: int, excl: int | None = None, reseed: int = 65536, threads: int = 0):
+    """TIER-B reference: the same self-join profile as selfjoin_brute for FULL
+    C3/C4-size series, by a plain multithreaded FP64 diagonal recurrence with exact re-seeding
+    every `reseed` rows (oracle/mp_tierb.c).  Pinned to selfjoin_brute; series with flat windows
+    are not supported.  Returns (P, I)."""
+    from ._clib import tierb_selfjoin
+    excl = (m + 1) // 2 if excl is None else excl
+    return tierb_selfjoin(r, m, excl, reseed, threads)
 
 
 # ------------------------------------------------------------------------------------------

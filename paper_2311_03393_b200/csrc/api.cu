@@ -614,7 +614,7 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   w.excl = excl;
   w.n_sub = n - cfg->m + 1;
   w.ldq = round_up(w.n_sub + join_pad(dtype), 64);
-  int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 8192 : 2048);
+  int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 16384 : 2048);
   if (cfg->reseed_rows <= 0) {
     // small problems: shorten the tiles until the grid has ~2 waves of 148 SMs x 16 warps
     const int64_t W = join_width(dtype);

@@ -2,9 +2,11 @@
 outputs the oracle computes one by one (SURVEY §8(c) "Parity contract"):
 
 * C3 (d=1000, n=1e5, FP32): sketch at sampled time columns; profile at sampled rows of every
-  series; every reported discord's score re-derived by the oracle;
+  series by brute force, and EVERY row of every series against the tier-B reference; every
+  reported discord's score re-derived by the oracle;
 * C4 (d=10,000, n=2e5, FP32) dynamic test: build, add 500, delete 500 (the bench step) -> the
-  sketch at sampled columns equals the oracle's sketch of the final stream set; sampled rows;
+  sketch at sampled columns equals the oracle's sketch of the final stream set; sampled rows,
+  and every row of 4 of the 64 series against the tier-B reference;
 * C5-shaped join (k=32, n=2e6, m=256, FP32): sampled rows, and bit-identical keys for a 2-band
   split (the multi-GPU decomposition).
 The oracle always works on its own sketch of the generator's streams (never on GPU output)."""
@@ -73,6 +75,31 @@ def _check_rows(R_or, P, I, m, rows_per_series, seed, tol=1e-3, extra_rows=None)
                 assert d <= Po[q] * (1 + tol) + floor * tol, (g, i, j, Io[q], d, Po[q])
 
 
+def _check_full_tierb(R_or, P, I, m, series, tol=1e-3, label=""):
+    """EVERY row of the listed series against the tier-B reference (the full
+    profile of the oracle's own sketch by the FP64 diagonal recurrence, pinned to the brute
+    force); index mismatches must be documented ties (the GPU's neighbour within tol)."""
+    excl = (m + 1) // 2
+    floor = 1e-3 * math.sqrt(m)
+    ties = 0
+    for g in series:
+        Pt, It = ref.selfjoin_tierb(R_or[g], m, excl)
+        err = np.abs(P[g] - Pt) / np.maximum(Pt, floor)
+        assert err.max() <= tol, f"{label} g={g}: rel err {err.max():.2e} at row {int(np.argmax(err))}"
+        mism = np.where(I[g] != It)[0]
+        if len(mism):
+            mu, sig, _ = ref.window_stats(R_or[g], m)
+            for i in mism:
+                j = int(I[g, i])
+                assert abs(int(i) - j) > excl
+                zi = (R_or[g, i:i + m] - mu[i]) / sig[i]
+                zj = (R_or[g, j:j + m] - mu[j]) / sig[j]
+                d = float(np.sqrt(((zi - zj) ** 2).sum()))
+                assert d <= Pt[i] * (1 + tol) + floor * tol, (label, g, i, j, It[i], d, Pt[i])
+        ties += len(mism)
+    print(f"{label}: full profiles of {len(series)} series vs tier B, {ties} documented ties")
+
+
 def test_c3_full(cuda):
     import torch
     import paper_2311_03393_b200 as skmp
@@ -95,6 +122,7 @@ def test_c3_full(cuda):
     for d in top:
         extra.setdefault(d.g, []).append(d.t)
     _check_rows(R_or, Pn, In, cfg.m, 3, seed=33, extra_rows={k_: np.array(v) for k_, v in extra.items()})
+    _check_full_tierb(R_or, Pn, In, cfg.m, range(cfg.k), label="C3")   # all 32 x 99,873 rows
     for d in top:  # reported scores are the profile values, and the oracle agrees
         assert d.score == float(Pn[d.g, d.t])
         assert d.score == max(float(Pn[gg, d.t]) for gg in range(cfg.k) if not inert[gg])
@@ -129,7 +157,9 @@ def test_c4_dynamic_full(cuda):
     plan = skmp.sketch_plan(sk)
     assert sorted(plan["ids"].tolist()) == sorted(final_ids.tolist())
     R_or = _oracle_sketch_full(final_T, mu, sg, g, s, cfg.k)
-    _check_rows(R_or, P.cpu().numpy(), I.cpu().numpy(), cfg.m, 1, seed=44)
+    Pn, In = P.cpu().numpy(), I.cpu().numpy()
+    _check_rows(R_or, Pn, In, cfg.m, 1, seed=44)
+    _check_full_tierb(R_or, Pn, In, cfg.m, (0, 21, 42, 63), label="C4")  # every row of 4 series
 
 
 def test_c5_shape_join_and_bands(cuda):

@@ -370,3 +370,21 @@ def test_sketch_with_stored_stats_point_update_closed_form():
     want[:, 123] += S[:, 4] * 2.5 / sig_d[4]
     want[:, 5] += S[:, 7] * -1.25 / sig_d[7]
     np.testing.assert_allclose(Rdu, want, rtol=0, atol=1e-12 * np.abs(Rd).max())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tierb_recurrence_matches_brute_force(seed):
+    """Tier B: the FP64 diagonal recurrence with exact re-seeds equals the
+    explicit-difference brute force to 1e-10 relative, also across re-seed boundaries (a short
+    re-seed interval) and for several exclusion radii; indices equal up to exact-rho ties."""
+    rng = np.random.default_rng([seed, 41])
+    m = [16, 32, 50][seed % 3]
+    n = int(rng.integers(600, 1500))
+    r = synthgen.mp_series(1, n, seed=400 + seed, kind=["mix", "randwalk", "seasonal"][seed % 3])[0]
+    for excl, reseed in (((m + 1) // 2, 65536), ((m + 1) // 2, 37), (0, 100), (3 * m, 1)):
+        Pb, Ib, _ = ref.selfjoin_rows(r, m, excl)
+        Pt, It = ref.selfjoin_tierb(r, m, excl, reseed=reseed, threads=3)
+        np.testing.assert_allclose(Pt, Pb, rtol=1e-10, atol=0)
+        Z, _ = ref.znorm_windows(r, m)
+        for i in np.where(It != Ib)[0]:
+            assert abs(np.sqrt(((Z[i] - Z[It[i]]) ** 2).sum()) - Pb[i]) <= 1e-10 * Pb[i]
