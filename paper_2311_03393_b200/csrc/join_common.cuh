@@ -201,22 +201,6 @@ __device__ __forceinline__ void publish(int64_t* keys, int64_t i, double v, int6
   }
 }
 
-// Warp-wide best candidate of ONE profile entry (all lanes hold candidates for the same row):
-// larger value, then smaller set base (reading 8); the result lands in every lane, so one
-// atomic per row replaces up to 32 contending ones (decisive for the FP64 128-bit CAS).
-template <typename T>
-__device__ __forceinline__ void warp_best(T& v, int64_t& b) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const T ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int64_t ob = __shfl_xor_sync(0xffffffffu, b, o);
-    if (ov > v || (ov == v && ob < b)) {
-      v = ov;
-      b = ob;
-    }
-  }
-}
-
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");

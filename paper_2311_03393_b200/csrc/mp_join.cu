@@ -49,17 +49,12 @@ template <typename T, int D>
 SKMP_PUB_ATTR void publish_pair(int64_t* keys, int64_t* keysc, typename JT<T>::Q* rowq, T* cthr, int rb_u,
                                           int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
                                           T colv0, T colv1) {
-  // rows i_u, i_u + 1 are shared by the warp's lanes: reduce first, publish once per row
-  int64_t ba = i_u + dt, bb = i_u + 1 + dt;
-  warp_best(rowa, ba);
-  warp_best(rowb, bb);
-  const bool lead = (threadIdx.x & 31) == 0;
-  if (lead && rowa >= rowq[rb_u].w) {
-    publish(keys, i_u, rowa, ba);
+  if (rowa >= rowq[rb_u].w) {
+    publish(keys, i_u, rowa, i_u + dt);
     rowq[rb_u].w = rowa;
   }
-  if (lead && rowb >= rowq[rb_u + 1].w) {
-    publish(keys, i_u + 1, rowb, bb);
+  if (rowb >= rowq[rb_u + 1].w) {
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt);
     rowq[rb_u + 1].w = rowb;
   }
   if (colv0 >= cthr[ct0]) {

@@ -119,18 +119,13 @@ SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, int64_t* keysc, Smem* sm, int rb
                                         int64_t i_u, int64_t dt, float rowaA, float rowaB,
                                         float rowbA, float rowbB, float cA0, float cA1, float cB0,
                                         float cB1) {
-  // rows i_u, i_u + 1 are shared by the warp's lanes: reduce first, publish once per row
-  float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
-  int64_t ba = i_u + dt + (rowaB > rowaA ? H : 0), bb = i_u + 1 + dt + (rowbB > rowbA ? H : 0);
-  warp_best(rowa, ba);
-  warp_best(rowb, bb);
-  const bool lead = (threadIdx.x & 31) == 0;
-  if (lead && rowa >= sm->rthr[rbu]) {
-    publish(keys, i_u, rowa, ba);
+  const float rowa = max2(rowaA, rowaB), rowb = max2(rowbA, rowbB);
+  if (rowa >= sm->rthr[rbu]) {
+    publish(keys, i_u, rowa, i_u + dt + (rowaB > rowaA ? H : 0));
     sm->rthr[rbu] = rowa;
   }
-  if (lead && rowb >= sm->rthr[rbu + 1]) {
-    publish(keys, i_u + 1, rowb, bb);
+  if (rowb >= sm->rthr[rbu + 1]) {
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt + (rowbB > rowbA ? H : 0));
     sm->rthr[rbu + 1] = rowb;
   }
   // columns c = i + dt (A) and c + H (B) complete after row i: their rows are [i - DG + 1, i]
