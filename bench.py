@@ -257,10 +257,17 @@ def main():
     cells_band = k * ((b0 - a0) * n_sub - (b0 * (b0 - 1) - a0 * (a0 - 1)) // 2)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    S_dense = synthgen.dense_S(cfg)[:, [int(j) for j in my_ids]] if cfg.proj == "dense" else None
+
+    def build(T):
+        if S_dense is not None:  # C1's Gaussian projection (reading 1)
+            return skmp.sketch_build(T, my_ids, k, proj=skmp.PROJ_DENSE, S=S_dense)
+        return skmp.sketch_build(T, my_ids, k, seed=cfg.seed)
+
     def step(T, Ta, Tdl, timers=None):
         e = [ev() for _ in range(7)] if timers is not None else None
         if e: e[0].record()
-        sk = skmp.sketch_build(T, my_ids, k, seed=cfg.seed)
+        sk = build(T)
         if e: e[1].record()
         if Ta is not None:
             skmp.sketch_add_dim(sk, Ta, my_add)
@@ -355,7 +362,7 @@ def main():
     if not args.no_e2e and host_T is not None:
         step(host_T, host_add, host_del)  # warm the staging pool
         # members of the top discord's group (the streams Alg. 3 stages each step), all ranks
-        gsk = skmp.sketch_build(Td, my_ids, k, seed=cfg.seed)
+        gsk = build(Td)
         if Tadd is not None:
             skmp.sketch_add_dim(gsk, Tadd, my_add)
         if Tdel is not None:
