@@ -121,6 +121,18 @@ struct MpDev {
   int64_t* keys;              // k x n_sub x words
   int32_t* flat_list;         // k x n_sub (only filled for series with nflat > 0)
 };
+// series per join chunk: as many as keep the chunk's operand records, window means and keys
+// (row and column side) within ~48 MB of the 126 MB L2
+inline int join_series_chunk(const MpDev& wr, const MpDev& wc) {
+  const double rec = wr.dtype == SKMP_F32 ? 16.0 : 32.0;
+  const double words = wr.dtype == SKMP_F32 ? 8.0 : 16.0;
+  auto side = [&](const MpDev& w) { return (rec + 8.0) * (double)w.ldq + words * (double)w.n_sub; };
+  const double per = side(wr) + (&wr == &wc ? 0.0 : side(wc));
+  int G = (int)(48.0e6 / per);
+  if (G < 1) G = 1;
+  if (G > wr.k) G = wr.k;
+  return G;
+}
 cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st);
 cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st);
 // band join of row series w against column series wc (the same workspace for a self-join):

@@ -58,7 +58,8 @@ struct JoinArgs {
   const int64_t* prefix;  // nblk + 1 cumulative tile counts
   int64_t nblk;
   int64_t blk0;
-  int k;                  // series (the grid enumerates tiles of all series, block-major)
+  int k;                  // series
+  int G;                  // series per L2-resident chunk (tile order: chunk, block, series, row)
 };
 
 inline JoinArgs make_join_args(const MpDev& wr, const MpDev& wc, int64_t dlo, int64_t dhi,
@@ -88,6 +89,7 @@ inline JoinArgs make_join_args(const MpDev& wr, const MpDev& wc, int64_t dlo, in
   a.nblk = nblk;
   a.blk0 = blk0;
   a.k = wr.k;
+  a.G = join_series_chunk(wr, wc);
   return a;
 }
 
@@ -210,23 +212,28 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 
-// Tile of the band this CTA owns.  Launch order is diagonal-block-major across ALL series
-// (block b's tiles of series 0, 1, ..., k-1, then block b+1 ...): the nearest diagonals of every
-// series run first, so the profile thresholds are good early and later tiles publish rarely.
-// Global tile T lies in block b with prefix[b] k <= T < prefix[b+1] k (binary search).
+// Tile of the band this CTA owns.  Launch order: series are taken in chunks of G whose operand
+// records and keys fit in L2 together (join_series_chunk); inside a chunk the order is
+// diagonal-block-major (block b of every series of the chunk before block b+1), so every
+// profile gets its near-diagonal candidates early and later tiles rarely pass the publish
+// check, while the chunk's working set stays L2-resident.
 __device__ __forceinline__ void decode_tile(const JoinArgs& a, int64_t W, int k, int* g, int64_t* delta0,
                                             int64_t* i0, int64_t* i1) {
-  const int64_t tile = blockIdx.x;
+  const int64_t per = a.prefix[a.nblk];       // row tiles of one series over the whole band
+  const int64_t chunk = (int64_t)blockIdx.x / (per * a.G);
+  const int c0 = (int)(chunk * a.G);
+  const int kc = (k - c0 < a.G) ? k - c0 : a.G;
+  const int64_t tile = (int64_t)blockIdx.x - chunk * per * a.G;
   int64_t lo = 0, hi = a.nblk - 1;
   while (lo < hi) {
     const int64_t mid = (lo + hi + 1) >> 1;
-    if (a.prefix[mid] * k <= tile) lo = mid; else hi = mid - 1;
+    if (a.prefix[mid] * kc <= tile) lo = mid; else hi = mid - 1;
   }
   const int64_t b = lo;
   const int64_t nb = a.prefix[b + 1] - a.prefix[b];  // row tiles of block b (per series)
-  const int64_t local = tile - a.prefix[b] * k;
-  *g = (int)(local / nb);
-  const int64_t rt = local - (int64_t)(*g) * nb;
+  const int64_t local = tile - a.prefix[b] * kc;
+  *g = c0 + (int)(local / nb);
+  const int64_t rt = local - (int64_t)(*g - c0) * nb;
   *delta0 = (a.blk0 + b) * W;
   const int64_t dmin = *delta0 > a.dlo ? *delta0 : a.dlo;
   const int64_t rows = tile_rows(a.n_sub, a.n_sub_c, dmin);

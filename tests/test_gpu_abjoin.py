@@ -136,3 +136,10 @@ def test_alg2_time_detection_train_test(cuda):
     C, G = ref.combine(Po, inert_o)
     want = ref.topk_greedy(C, G, Io, 6, (cfg.m + 1) // 2)
     check_topk(top, want, C, TOL["f64"], label="alg2 train/test")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mp_abjoin_long_windows(cuda, dtype):
+    A = synthgen.mp_series(1, 1800, seed=91, kind="mix")
+    B = synthgen.mp_series(1, 2500, seed=92, kind="seasonal")
+    _run(cuda, A, B, 300, dtype, label=f"m=300 {dtype}")

@@ -147,3 +147,13 @@ def test_mp_finalize_rows_slices(cuda, dtype):
     with pytest.raises(skmp.SkmpError):
         skmp.mp_finalize_rows(w, 5, n_sub + 1)
     w.free()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mp_long_windows(cuda, dtype):
+    """m larger than the finalize staging chunk (256 windows positions): the set resolution and
+    the explicit-difference distance run over several staged chunks / from global memory."""
+    X = synthgen.mp_series(2, 3000, seed=81, kind="mix")
+    _run(cuda, X, 600, dtype, reseed=256, label=f"m=600 {dtype}")
+    X = synthgen.mp_series(1, 2200, seed=82, kind="randwalk")
+    _run(cuda, X, 257, dtype, label=f"m=257 {dtype}")
