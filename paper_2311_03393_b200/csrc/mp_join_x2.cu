@@ -1,9 +1,11 @@
-// K6 (FP32): the self-join hot loop on Blackwell's packed FP32 pipe (FFMA2 / FMUL2).
+// K6 (FP32, the default FP32 join): the join hot loop on Blackwell's packed FP32 instructions
+// (FFMA2 / FMUL2).  Self-join and both AB-join passes (row / column series, JoinArgs).
 //
 // Same method as mp_join.cu (Def. 6, self-join P:L322; STOMP/SCAMP recurrence
 //   cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i,  rho = cov inv_i inv_j)
 // but every arithmetic instruction of the recurrence works on TWO diagonals at once
-// (`fma.rn.f32x2`, sm_100+), halving the issue slots the FP32 arithmetic needs:
+// (`fma.rn.f32x2`, sm_100+), halving the issue slots the FP32 arithmetic needs (not the FMA-pipe
+// time: an FFMA2 occupies the pipe for two cycles, tools/micro/pipe_mix.cu):
 //  * thread t owns two groups of DG diagonals, group A = [delta0 + t DG, +DG) and group B = the
 //    same + H (H = 32 DG, half the tile width W = 2H); slot d of both groups lives in one 64-bit
 //    register pair, so cov, the column operands and the keys are all f32x2;
