@@ -157,3 +157,14 @@ def test_mp_long_windows(cuda, dtype):
     _run(cuda, X, 600, dtype, reseed=256, label=f"m=600 {dtype}")
     X = synthgen.mp_series(1, 2200, seed=82, kind="randwalk")
     _run(cuda, X, 257, dtype, label=f"m=257 {dtype}")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_mp_minimal_admissible_size(cuda, dtype):
+    """n_sub = 2 excl + 2: the two end rows have exactly one admissible neighbour each (each
+    other) and every row has at least one (reading 16)."""
+    for m in (8, 33):
+        excl = (m + 1) // 2
+        n = 2 * excl + 2 + m - 1
+        X = synthgen.mp_series(2, n, seed=100 + m, kind="noise")
+        _run(cuda, X, m, dtype, label=f"minimal m={m}")
