@@ -45,6 +45,10 @@ constexpr int kJoinD64 = SKMP_JOIN_D64;  // diagonals per thread of the FP64 joi
 #define SKMP_JOIN_C 32
 #endif
 constexpr int kJoinC = SKMP_JOIN_C;  // rows per staged chunk (power of two, multiple of 2D)
+#ifndef SKMP_X2_C
+#define SKMP_X2_C 32
+#endif
+constexpr int kJoinCx2 = SKMP_X2_C;  // rows per staged chunk of the packed FP32 join
 int join_d32();                // diagonals per thread of the FP32 join (env SKMP_JOIN_D: 8 | 16)
 bool join_x2_enabled();        // packed f32x2 FP32 join (default; SKMP_JOIN_IMPL=scalar disables)
 int join_x2_width();           // its tile width
@@ -68,7 +72,9 @@ inline __host__ __device__ int64_t tile_rows(int64_t n_sub_r, int64_t n_sub_c, i
 // FP32 profile keys store (candidate-set base + kKeyArgBias) so that bases down to -(D-1) fit
 constexpr int64_t kKeyArgBias = 32;
 // padding (in windows) behind n_sub in the prepared arrays so tile loops may over-read
-inline int64_t join_pad(int dtype) { return join_width(dtype) + 4 * kJoinC + 64; }
+inline int64_t join_pad(int dtype) {
+  return join_width(dtype) + 4 * (kJoinC > kJoinCx2 ? kJoinC : kJoinCx2) + 64;
+}
 
 // ------------------------------------------------------------------------------------------
 // stream-statistics (K1) and projection (K2/K2d/K3) launchers — sketch.cu

@@ -47,10 +47,11 @@ constexpr int NT = 32;            // one warp per CTA
 constexpr int DG = SKMP_X2_DG;    // diagonals per group per thread (2 DG cells per row)
 constexpr int H = NT * DG;        // 128: group B offset; tile width W = 2H
 constexpr int W = 2 * H;
-constexpr int C = kJoinC;         // rows per staged chunk
+constexpr int C = kJoinCx2;       // rows per staged chunk
+constexpr int CPT = C / NT;       // rows / column records each thread stages per chunk
 constexpr int RS = H + 2 * C;     // ring records
 constexpr int RSD = RS / DG;
-static_assert(RS % DG == 0 && C % (2 * DG) == 0 && (C & (C - 1)) == 0 && C == NT, "geometry");
+static_assert(RS % DG == 0 && C % (2 * DG) == 0 && (C & (C - 1)) == 0 && C % NT == 0, "geometry");
 
 // ---- f32x2 helpers (64-bit register pairs) ----------------------------------------------------
 typedef unsigned long long f2;
@@ -369,10 +370,10 @@ join_x2_kernel(JoinArgs a) {
     fetch_col(cs, qc, keysc, i0 + delta0 + e, n_sub_c);
     land_col(cs, &sm, i0 + delta0 + e);
   }
-  {
+  for (int e = tid; e < C; e += NT) {
     RowStage rs;
-    fetch_row(rs, q, keys, i0 + tid, n_sub);
-    land_row(rs, &sm, i0 + tid);
+    fetch_row(rs, q, keys, i0 + e, n_sub);
+    land_row(rs, &sm, i0 + e);
   }
   __syncwarp();
 
@@ -387,7 +388,12 @@ join_x2_kernel(JoinArgs a) {
   for (int64_t r = i0; r < i1; r += C) {
     const int64_t rend = (r + C < i1) ? r + C : i1;
     const bool more = r + C < i1;
-    if (more) stage_next(&sm, q, keys, qc, keysc, r + delta0 + H + C + tid, r + C + tid, n_sub, n_sub_c, tid);
+    if (more) {
+#pragma unroll
+      for (int p = 0; p < CPT; ++p)
+        stage_next(&sm, q, keys, qc, keysc, r + delta0 + H + C + tid + p * NT, r + C + tid + p * NT, n_sub,
+                   n_sub_c, tid + p * NT);
+    }
     const int nrot = (int)((rend - r) / DG);
     int rb = (int)(r & (2 * C - 1));
     int64_t ib = r;
@@ -403,7 +409,8 @@ join_x2_kernel(JoinArgs a) {
     }
     if (more) {
       cp_async_wait_all();
-      land_next(&sm, r + delta0 + H + C + tid, r + C + tid, tid);
+#pragma unroll
+      for (int p = 0; p < CPT; ++p) land_next(&sm, r + delta0 + H + C + tid + p * NT, r + C + tid + p * NT, tid + p * NT);
     }
     __syncwarp();
   }
