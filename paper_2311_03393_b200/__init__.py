@@ -8,6 +8,7 @@ PyTorch supplies device memory and the current CUDA stream.  The same names as t
     sketch_plan, sketch_refresh, sketch_free, mp_create, mp_join, mp_keys, mp_band, mp_finalize,
     mp_finalize_rows, mp_free,
     mp_selfjoin, mp_abjoin, discord_topk, discord_dims
+plus Python-level compositions of those calls: group_rows, detect_dimension, detect.
 
 There is no CPU fallback: if the shared library is missing, `lib()` raises; compute calls
 without a GPU return SKMP_E_CUDA (raised as SkmpError).
@@ -494,4 +495,52 @@ def detect_dimension(sk: Sketch, sources, t: int, g: int, m: int, excl: int = -1
             if best is None or cand[:2] > best[:2]:
                 best = cand
     return None if best is None else (best[2], best[0], best[3])
+
+
+@dataclass
+class DiscordReport:
+    """The paper's detection output (Alg. 2 + Alg. 3 + optional refinement)."""
+    t: int                 # discord time i* (Alg. 2, combined sketch profile)
+    g: int                 # discord group g*
+    score: float           # sketched discord score C[i*]
+    j_id: int              # dimension j* (stream id, Alg. 3)
+    j_score: float         # 1NN distance of T_{j*, i*, m} in its own stream
+    j_nn: int              # its nearest neighbour's time
+    refined_t: int | None  # top-1 discord of the full profile of stream j* (P:L303-304)
+    refined_score: float | None
+    ms: dict               # per-phase device times
+
+
+def detect(T, ids, k: int, m: int, *, seed: int = 0, proj: int = PROJ_COUNT_SKETCH, S=None,
+           refine: bool = True, stream=None) -> DiscordReport:
+    """End-to-end single-series mode over the C-ABI: Alg. 1 sketch -> self-join of every
+    sketch series -> Alg. 2 combine / top-1 -> Alg. 3 over J_g* -> optional refinement join.
+    T: d x n CUDA tensor (rows = streams with `ids`)."""
+    import torch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record()
+    if proj == PROJ_DENSE:
+        sk = sketch_build(T, ids, k, proj=PROJ_DENSE, S=S, stream=stream)
+    else:
+        sk = sketch_build(T, ids, k, seed=seed, stream=stream)
+    ev[1].record()
+    P, I, inert = mp_selfjoin(sk.R, m, stream=stream)
+    top = discord_topk(P, I, inert, m=m, top=1, stream=stream)[0]
+    ev[2].record()
+    rows = group_rows(sk, top.g)
+    sc, nn, js = discord_dims(T, rows, top.t, m, stream=stream)
+    ev[3].record()
+    j = int(rows[js])
+    rt = rs = None
+    if refine:
+        Pj, _, _ = mp_selfjoin(T[j:j + 1], m, stream=stream)
+        rt = int(torch.argmax(Pj[0]))
+        rs = float(Pj[0, rt])
+    ev[4].record()
+    torch.cuda.synchronize()
+    ids_a = np.asarray(ids)
+    sk.free()
+    ms = {"sketch": ev[0].elapsed_time(ev[1]), "time_detection": ev[1].elapsed_time(ev[2]),
+          "dimension_detection": ev[2].elapsed_time(ev[3]), "refine": ev[3].elapsed_time(ev[4])}
+    return DiscordReport(top.t, top.g, top.score, int(ids_a[j]), float(sc[js]), int(nn[js]), rt, rs, ms)
 

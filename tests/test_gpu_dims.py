@@ -164,3 +164,24 @@ def test_detect_dimension_after_add_delete(cuda):
     sc, nn, js = ref.dimension_detection(M, list(range(len(members))), t_star, cfg.m)
     assert got[0] == members[js] and abs(got[1] - sc[js]) <= 1e-9 * sc[js] and got[2] == nn[js]
     assert all(j not in members for j in dele.tolist())
+
+
+def test_detect_report_matches_oracle_pipeline(cuda):
+    """skmp.detect (Alg. 1 -> Alg. 2 -> Alg. 3 -> refinement, single-series mode
+    P:L322) on C2 against the oracle's pipeline."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.CONFIGS["c2"]
+    T = synthgen.streams(cfg)
+    ids = synthgen.stream_ids(cfg)
+    rep = skmp.detect(torch.from_numpy(T).to(cuda), ids, cfg.k, cfg.m, seed=cfg.seed)
+    g, s = plan_count_sketch(ids, cfg.k, cfg.seed)
+    o = ref.detect(T, cfg.k, cfg.m, 1, groups=g, signs=s)
+    t_o, g_o, _, c_o = o["top"][0]
+    assert (rep.t, rep.g) == (t_o, g_o) and abs(rep.score - c_o) <= 1e-9 * c_o
+    rows = [q for q in range(cfg.d) if g[q] == g_o]
+    so, no, jo = ref.dimension_detection(T, rows, t_o, cfg.m)
+    assert rep.j_id == int(ids[rows[jo]]) and abs(rep.j_score - so[jo]) <= 1e-9 * so[jo]
+    t_r, _, s_r, _, _ = ref.refine(T[rows[jo]], cfg.m)
+    assert rep.refined_t == t_r and abs(rep.refined_score - s_r) <= 1e-9 * s_r
+    assert set(rep.ms) == {"sketch", "time_detection", "dimension_detection", "refine"}
