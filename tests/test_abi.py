@@ -84,3 +84,37 @@ def test_compute_calls_fail_loudly_without_gpu():
     with pytest.raises(skmp.SkmpError) as e:
         skmp.sketch_build(T, np.arange(3), 2, seed=1)
     assert e.value.name == "SKMP_E_CUDA"
+
+
+def test_argument_validation_before_any_device_work():
+    """Validation precedes the device check (ABI rule: errors before any launch): these fail with
+    the argument error, not SKMP_E_CUDA, even without a GPU."""
+    import torch
+    T = np.random.default_rng(1).standard_normal((3, 100))
+    cases = [
+        (lambda: skmp.discord_dims(T, [0], 100 - 16 + 1, 16), "SKMP_E_INVALID_ARG"),    # t* past the end
+        (lambda: skmp.discord_dims(T, [-1], 0, 16), "SKMP_E_INVALID_ARG"),              # negative row
+        (lambda: skmp.discord_dims(T, [0], 40, 16, 60), "SKMP_E_NO_ADMISSIBLE"),        # excl too wide
+        (lambda: skmp.discord_dims(T[:, :10].copy(), [0], 0, 16), "SKMP_E_SERIES_TOO_SHORT"),
+    ]
+    for fn, name in cases:
+        with pytest.raises(skmp.SkmpError) as e:
+            fn()
+        assert e.value.name == name
+    if not torch.cuda.is_available():
+        with pytest.raises(skmp.SkmpError) as e:
+            skmp.discord_dims(T, [0, 2], 10, 16)
+        assert e.value.name == "SKMP_E_CUDA"   # valid arguments: then no device -> loud failure
+
+
+def test_abjoin_argument_validation():
+    L = skmp.lib()
+    cfg = skmp._mpcfg(16)
+    buf = (ctypes.c_double * 4)()
+    i64 = (ctypes.c_int64 * 4)()
+    # NULL outputs / too-short series rejected before any device work
+    assert L.mp_abjoin(ctypes.cast(buf, ctypes.c_void_p), 100, 100, ctypes.cast(buf, ctypes.c_void_p), 100, 100, 1, 1,
+                       ctypes.byref(cfg), None, None, None, None, None, None) == 1
+    assert L.mp_abjoin(ctypes.cast(buf, ctypes.c_void_p), 10, 10, ctypes.cast(buf, ctypes.c_void_p), 100, 100, 1, 1,
+                       ctypes.byref(cfg), ctypes.cast(buf, ctypes.c_void_p), ctypes.cast(i64, ctypes.c_void_p),
+                       None, None, None, None) == 4
