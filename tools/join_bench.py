@@ -12,9 +12,26 @@ ap.add_argument("--m", type=int, default=256)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--reseed", type=int, default=0)
+ap.add_argument("--ab", type=int, default=0, help="AB-join: test length nA (train = --n)")
 a = ap.parse_args()
 dt = torch.float32 if a.dtype == "f32" else torch.float64
 R = synthgen.mp_series_torch(a.k, a.n, 7, "cuda", dt)
+if a.ab:
+    RA = synthgen.mp_series_torch(a.k, a.ab, 8, "cuda", dt)
+    cells = a.k * (a.ab - a.m + 1) * (a.n - a.m + 1)
+    skmp.mp_abjoin(RA, R, a.m, reseed_rows=a.reseed, both=True)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); skmp.mp_abjoin(RA, R, a.m, reseed_rows=a.reseed, both=True); e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = min(ts)
+    lanes = 128 if a.dtype == "f32" else 64
+    print(f"AB-join k={a.k} nA={a.ab} nB={a.n} m={a.m} {a.dtype}: {t:.2f} ms (create + both passes + both finalizes), "
+          f"{cells / t * 1e3:.3e} cells/s, pipe {cells / t * 1e3 * 4 / (148 * lanes * 1.965e9):.3f}")
+    sys.exit(0)
 n_sub = a.n - a.m + 1
 excl = (a.m + 1) // 2
 aa = n_sub - excl - 1
