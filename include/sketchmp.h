@@ -234,6 +234,31 @@ skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, i
                       int32_t k, int32_t dtype, const skmp_mp_cfg* cfg, void* PA, int64_t* IA, void* PB,
                       int64_t* IB, uint8_t* inert, void* stream);
 
+/* The AB-join in stages, for its multi-GPU decomposition (the same diagonal-band scheme as the
+ * self-join):
+ *  mp_create_ab   as mp_create, but an AB workspace: no exclusion zone, no NO_ADMISSIBLE check;
+ *  mp_join_ab     cells (i, i + delta), i a window of `rows`, i + delta a window of `cols`,
+ *                 delta in [diag_lo, diag_hi) (clipped to cols' windows); pass 1 of Def. 6's
+ *                 AB-join is (rows = test, cols = train, delta >= 0), pass 2 (rows = train,
+ *                 cols = test, delta >= 1); row candidates go to `rows`' keys, column candidates
+ *                 to `cols`' keys; any split of the two passes into bands accumulates bit-identical
+ *                 keys (keys reduce across GPUs with mp_keys exactly as for the self-join);
+ *  mp_finalize_ab windows [row_lo, row_hi) (0, 0 -> all) of `w` resolved against `other`'s windows
+ *                 (PA, IA of mp_abjoin for w = test), full-size P / I [dev], inert [host] k or NULL;
+ *  mp_abband      host-only: band `band` of `nbands` equal-cell bands of the two passes taken as
+ *                 one sequence (pass 1 diagonals 0 .. n_subB-1, then pass 2 diagonals 1 ..
+ *                 n_subA-1), edges on the tile grid; a band may hold a piece of each pass:
+ *                 [lo1, hi1) of pass 1 and [lo2, hi2) of pass 2 (empty ranges as lo == hi).
+ * Errors: INVALID_ARG (NULL, workspaces not from mp_create_ab, mismatched k / dtype / m, bad
+ * bands or rows), SERIES_TOO_SHORT, CUDA, OOM.  mp_join_ab is asynchronous. */
+skmp_status mp_create_ab(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                         const skmp_mp_cfg* cfg, void* stream, skmp_mp** out);
+skmp_status mp_join_ab(skmp_mp* rows, skmp_mp* cols, int64_t diag_lo, int64_t diag_hi, void* stream);
+skmp_status mp_finalize_ab(skmp_mp* w, skmp_mp* other, int64_t row_lo, int64_t row_hi, void* P, int64_t* I,
+                           uint8_t* inert, void* stream);
+skmp_status mp_abband(int64_t n_subA, int64_t n_subB, int32_t dtype, int32_t nbands, int32_t band,
+                      int64_t* lo1, int64_t* hi1, int64_t* lo2, int64_t* hi2);
+
 /* ---------------------------------------------------------------------------------------------
  * Discord detection over the sketch profiles: Alg. 2 Time-Detection + ordered
  * top-K list (reading 12):

@@ -90,6 +90,11 @@ _SIGS = {
                                     _P, _P]),
     "mp_abjoin": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _I64, _I32, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P,
                                  _P, _P]),
+    "mp_create_ab": (ctypes.c_int, [_P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, ctypes.POINTER(_P)]),
+    "mp_join_ab": (ctypes.c_int, [_P, _P, _I64, _I64, _P]),
+    "mp_finalize_ab": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "mp_abband": (ctypes.c_int, [_I64, _I64, _I32, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                 ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
 }
 
@@ -385,6 +390,46 @@ def mp_finalize_rows(w: MpWorkspace, row_lo: int, row_hi: int, P=None, I=None, s
         I = torch.zeros((w.k, w.n_sub), dtype=torch.int64, device="cuda")
     inert = np.zeros(w.k, dtype=np.uint8)
     _check(lib().mp_finalize_rows(w.handle, row_lo, row_hi, _ptr(P), _ptr(I), _ptr(inert), _stream(stream)))
+    return P, I, inert.astype(bool)
+
+
+def mp_abband(n_subA: int, n_subB: int, dtype: int, nbands: int, band: int):
+    """Band `band` of `nbands` equal-cell bands of the AB-join's two passes: ((lo1, hi1) of pass 1,
+    (lo2, hi2) of pass 2), diagonal ranges (empty as lo == hi)."""
+    v = [_I64() for _ in range(4)]
+    _check(lib().mp_abband(n_subA, n_subB, dtype, nbands, band, *[ctypes.byref(x) for x in v]))
+    return (v[0].value, v[1].value), (v[2].value, v[3].value)
+
+
+def mp_create_ab(R, m: int, *, reseed_rows: int = 0, stream=None) -> MpWorkspace:
+    """AB workspace of one side (k x n CUDA tensor) for the staged AB-join."""
+    k, n = R.shape
+    dt = _dtype_code(R)
+    cfg = _mpcfg(m, -1, reseed_rows)
+    h = ctypes.c_void_p()
+    _check(lib().mp_create_ab(_ptr(R), k, n, R.stride(0), dt, ctypes.byref(cfg), _stream(stream), ctypes.byref(h)))
+    return MpWorkspace(h, k, n - m + 1, dt)
+
+
+def mp_join_ab(rows: MpWorkspace, cols: MpWorkspace, diag_lo: int, diag_hi: int, stream=None):
+    """Cells (i, i + delta), delta in [diag_lo, diag_hi): pass 1 = (test, train), pass 2 = (train, test)
+    with delta >= 1."""
+    _check(lib().mp_join_ab(rows.handle, cols.handle, diag_lo, diag_hi, _stream(stream)))
+
+
+def mp_finalize_ab(w: MpWorkspace, other: MpWorkspace, row_lo: int = 0, row_hi: int = 0, P=None, I=None,
+                   stream=None):
+    """Profile of w's windows [row_lo, row_hi) (0, 0 -> all) against other's windows; P / I are
+    allocated zero-filled when not given (per-rank slices sum-reduce)."""
+    import torch
+    tdt = torch.float32 if w.dtype == F32 else torch.float64
+    if P is None:
+        P = torch.zeros((w.k, w.n_sub), dtype=tdt, device="cuda")
+    if I is None:
+        I = torch.zeros((w.k, w.n_sub), dtype=torch.int64, device="cuda")
+    inert = np.zeros(w.k, dtype=np.uint8)
+    _check(lib().mp_finalize_ab(w.handle, other.handle, row_lo, row_hi, _ptr(P), _ptr(I), _ptr(inert),
+                                _stream(stream)))
     return P, I, inert.astype(bool)
 
 

@@ -758,6 +758,7 @@ skmp_status mp_join(skmp_mp* h, int64_t diag_lo, int64_t diag_hi, void* stream) 
   if (diag_lo < 0 || diag_hi < 0 || (diag_hi < diag_lo))
     return set_error(SKMP_E_INVALID_ARG, "mp_join: bad diagonal band");
   MpDev& w = h->w;
+  if (w.excl < 0) return set_error(SKMP_E_INVALID_ARG, "mp_join: AB workspace; use mp_join_ab");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t lo = diag_lo, hi = diag_hi;
   if (lo == 0 && hi == 0) hi = w.n_sub;
@@ -781,6 +782,7 @@ skmp_status mp_keys(skmp_mp* h, void** keys, int64_t* count, int32_t* words) {
 
 skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* stream) {
   if (!h || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize: NULL argument");
+  if (h->w.excl < 0) return set_error(SKMP_E_INVALID_ARG, "mp_finalize: AB workspace; use mp_finalize_ab");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SKMP_CUDA(launch_mp_finalize(h->w, h->w, h->w.excl, P, I, st));
   if (inert) memcpy(inert, h->inert.data(), h->inert.size());
@@ -791,6 +793,7 @@ skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* s
 skmp_status mp_finalize_rows(skmp_mp* h, int64_t row_lo, int64_t row_hi, void* P, int64_t* I,
                              uint8_t* inert, void* stream) {
   if (!h || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: NULL argument");
+  if (h->w.excl < 0) return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: AB workspace; use mp_finalize_ab");
   if (row_lo < 0 || row_hi < row_lo || row_hi > h->w.n_sub)
     return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: need 0 <= row_lo <= row_hi <= n_sub");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -817,6 +820,100 @@ skmp_status mp_selfjoin(const void* R, int32_t k, int64_t n, int64_t ld, int32_t
   if (s == SKMP_OK) s = mp_finalize(h, P, I, inert, stream);
   mp_free(h);
   return s;
+}
+
+skmp_status mp_create_ab(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                         const skmp_mp_cfg* cfg, void* stream, skmp_mp** out) {
+  return mp_create_impl(R, k, n, ld, dtype, cfg, stream, out, true);
+}
+
+skmp_status mp_join_ab(skmp_mp* rows, skmp_mp* cols, int64_t diag_lo, int64_t diag_hi, void* stream) {
+  if (!rows || !cols) return set_error(SKMP_E_INVALID_ARG, "mp_join_ab: NULL workspace");
+  if (rows->w.excl >= 0 || cols->w.excl >= 0)
+    return set_error(SKMP_E_INVALID_ARG, "mp_join_ab: workspaces must come from mp_create_ab");
+  if (rows->w.k != cols->w.k || rows->w.dtype != cols->w.dtype || rows->w.m != cols->w.m)
+    return set_error(SKMP_E_INVALID_ARG, "mp_join_ab: k / dtype / m differ");
+  if (diag_lo < 0 || diag_hi < diag_lo) return set_error(SKMP_E_INVALID_ARG, "mp_join_ab: bad diagonal band");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t hi = std::min(diag_hi, cols->w.n_sub);
+  skmp_status s = join_band(rows->w, cols->w, diag_lo, hi, st);
+  if (s) return s;
+  rows->st = cols->st = st;
+  return ok();
+}
+
+skmp_status mp_finalize_ab(skmp_mp* w, skmp_mp* other, int64_t row_lo, int64_t row_hi, void* P, int64_t* I,
+                           uint8_t* inert, void* stream) {
+  if (!w || !other || !P || !I) return set_error(SKMP_E_INVALID_ARG, "mp_finalize_ab: NULL argument");
+  if (w->w.excl >= 0 || other->w.excl >= 0)
+    return set_error(SKMP_E_INVALID_ARG, "mp_finalize_ab: workspaces must come from mp_create_ab");
+  if (row_lo == 0 && row_hi == 0) row_hi = w->w.n_sub;
+  if (row_lo < 0 || row_hi < row_lo || row_hi > w->w.n_sub)
+    return set_error(SKMP_E_INVALID_ARG, "mp_finalize_ab: need 0 <= row_lo <= row_hi <= n_sub");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SKMP_CUDA(launch_mp_finalize(w->w, other->w, -1, P, I, st, row_lo, row_hi));
+  if (inert)  // reading 22: inert when both series of the group are entirely flat
+    for (int g = 0; g < w->w.k; ++g) inert[g] = w->inert[(size_t)g] && other->inert[(size_t)g];
+  w->st = st;
+  return ok();
+}
+
+skmp_status mp_abband(int64_t n_subA, int64_t n_subB, int32_t dtype, int32_t nbands, int32_t band,
+                      int64_t* lo1, int64_t* hi1, int64_t* lo2, int64_t* hi2) {
+  if (n_subA < 1 || n_subB < 1 || nbands < 1 || band < 0 || band >= nbands || !lo1 || !hi1 || !lo2 || !hi2)
+    return set_error(SKMP_E_INVALID_ARG, "mp_abband: bad arguments");
+  const int64_t W = join_width(dtype == SKMP_F64 ? SKMP_F64 : SKMP_F32);
+  // the two passes as one sequence of diagonals: pass 1 delta in [0, n_subB) (min(n_subA,
+  // n_subB - delta) cells), then pass 2 delta in [1, n_subA) (min(n_subB, n_subA - delta) cells)
+  auto cum1 = [&](int64_t x) -> double {  // cells of pass-1 diagonals [0, x)
+    double c = 0.0;
+    const int64_t flat = std::max<int64_t>(0, std::min(x, n_subB - n_subA));  // delta < nB - nA: nA cells
+    c += (double)flat * (double)n_subA;
+    const int64_t a = std::max<int64_t>(flat, 0), b = x;  // cells nB - delta
+    if (b > a) c += (double)(b - a) * (double)n_subB - ((double)b * (b - 1) - (double)a * (a - 1)) / 2.0;
+    return c;
+  };
+  auto cum2 = [&](int64_t y) -> double {  // cells of pass-2 diagonals [1, y)
+    if (y <= 1) return 0.0;
+    double c = 0.0;
+    const int64_t flat_end = std::max<int64_t>(1, std::min(y, n_subA - n_subB));  // delta < nA - nB: nB cells
+    c += (double)(flat_end - 1) * (double)n_subB;
+    const int64_t a = flat_end, b = y;
+    if (b > a) c += (double)(b - a) * (double)n_subA - ((double)b * (b - 1) - (double)a * (a - 1)) / 2.0;
+    return c;
+  };
+  const double tot1 = cum1(n_subB), tot = tot1 + cum2(n_subA);
+  // edge p of the split as a position (pass, delta), rounded to the tile grid of its pass
+  auto edge = [&](int32_t p, int* pass, int64_t* delta) {
+    if (p <= 0) { *pass = 1; *delta = 0; return; }
+    if (p >= nbands) { *pass = 2; *delta = n_subA; return; }
+    const double target = tot * (double)p / (double)nbands;
+    if (target < tot1) {
+      int64_t lo = 0, hi = n_subB;
+      while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (cum1(mid) < target) lo = mid + 1; else hi = mid; }
+      *pass = 1;
+      *delta = std::min<int64_t>(n_subB, (lo + W / 2) / W * W);
+    } else {
+      int64_t lo = 1, hi = n_subA;
+      while (lo < hi) { const int64_t mid = (lo + hi) / 2; if (tot1 + cum2(mid) < target) lo = mid + 1; else hi = mid; }
+      *pass = 2;
+      *delta = std::max<int64_t>(1, std::min<int64_t>(n_subA, (lo + W / 2) / W * W));
+    }
+  };
+  int pa, pb;
+  int64_t da, db;
+  edge(band, &pa, &da);
+  edge(band + 1, &pb, &db);
+  *lo1 = *hi1 = *lo2 = *hi2 = 0;
+  if (pa == 1) {
+    *lo1 = da;
+    *hi1 = pb == 1 ? std::max(da, db) : n_subB;
+    if (pb == 2) { *lo2 = 1; *hi2 = std::max<int64_t>(1, db); }
+  } else {
+    *lo2 = std::max<int64_t>(1, da);
+    *hi2 = std::max(*lo2, db);
+  }
+  return ok();
 }
 
 skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, int64_t nB, int64_t ldB,

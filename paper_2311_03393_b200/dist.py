@@ -8,6 +8,9 @@ each rank joins its band into its own profile keys, which are max-all-reduced (F
 int64 MAX on {orderable rho, ~j}; FP64: MAX on the value word, then MAX on the index word among
 the ranks holding that value), after which any rank can finalize.
 
+AB-join: the same scheme over its two passes taken as one diagonal sequence (mp_abband); the
+keys of both sides are max-all-reduced and each side's windows are finalized in row slices.
+
 Only the collectives live here (torch.distributed: NCCL on GPUs, gloo in the CPU tests);
 every computation step is a C-ABI call into libsketchmp.so.
 """
@@ -18,8 +21,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (F32, F64, Sketch, detect_dimension, mp_band, mp_create, mp_finalize, mp_finalize_rows,
-               mp_join, mp_keys, sketch_refresh, sketch_view64)
+from . import (F32, F64, Sketch, detect_dimension, mp_abband, mp_band, mp_create, mp_create_ab, mp_finalize,
+               mp_finalize_ab, mp_finalize_rows, mp_join, mp_join_ab, mp_keys, sketch_refresh, sketch_view64)
 
 INT64_MIN = -(1 << 63)
 
@@ -120,3 +123,37 @@ def finalize_dist(w, group=None, dst: int = 0):
     dist.reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
     return (P, I, inert) if rank == dst else None
 
+
+
+def mp_abjoin_dist(RA: torch.Tensor, RB: torch.Tensor, m: int, *, reseed_rows: int = 0, both: bool = False,
+                   group=None, dst: int = 0):
+    """AB-join of RA (test) against RB (train), both replicated on every rank, its two passes split
+    into equal-cell diagonal bands over the ranks of `group` (mp_abband).  Keys of both sides
+    are max-reduced (a pass-2 band also feeds the test side's keys), then each rank finalizes a
+    slice of the test windows (and of the train windows with both=True), sum-reduced to `dst`.
+    Returns (PA, IA, inert) or (PA, IA, PB, IB, inert) on `dst`, None elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    a = mp_create_ab(RA, m, reseed_rows=reseed_rows)
+    b = mp_create_ab(RB, m, reseed_rows=reseed_rows)
+    (l1, h1), (l2, h2) = mp_abband(a.n_sub, b.n_sub, a.dtype, world, rank)
+    if l1 < h1:
+        mp_join_ab(a, b, l1, h1)   # pass 1: test rows, train columns
+    if l2 < h2:
+        mp_join_ab(b, a, l2, h2)   # pass 2: train rows, test columns
+    for w in ((a, b) if both else (a,)):
+        keys, words = mp_keys(w)
+        reduce_keys(keys, words, group)
+    out = []
+    inert = None
+    for w, o in ((a, b), (b, a)) if both else ((a, b),):
+        lo, hi = row_range(w.n_sub, world, rank)
+        if hi == 0:
+            lo = hi = w.n_sub   # empty slice ((0, 0) would mean all windows)
+        P, I, inert = mp_finalize_ab(w, o, lo, hi)
+        dist.reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
+        dist.reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
+        out += [P, I]
+    a.free()
+    b.free()
+    return (*out, inert) if rank == dst else None

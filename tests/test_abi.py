@@ -76,6 +76,56 @@ def test_band_partition(n_sub, excl, dtype):
             assert abs(cells(a, b) - tot / nb) <= W * n_sub + 1
 
 
+@pytest.mark.parametrize("nA,nB,dtype", [(199745, 199745, 0), (9901, 99873, 0), (99873, 9901, 0), (1951, 1951, 1),
+                                         (300, 5000, 1), (5000, 300, 0), (1, 1, 0), (7, 1, 1)])
+def test_abband_partition(nA, nB, dtype):
+    """The AB-join's two passes (pass 1 diagonals [0, nB), pass 2 diagonals [1, nA)) split into
+    equal-cell bands: every diagonal in exactly one band, interior edges on the tile grid,
+    balanced to within a tile width of cells."""
+    W = skmp.mp_tile_width(dtype)
+
+    def c1(a, b):  # cells of pass-1 diagonals [a, b): sum min(nA, nB - delta)
+        x = np.arange(a, b, dtype=np.float64)
+        return float(np.minimum(nA, nB - x).sum())
+
+    def c2(a, b):
+        x = np.arange(a, b, dtype=np.float64)
+        return float(np.minimum(nB, nA - x).sum())
+
+    assert c1(0, nB) + c2(1, nA) == float(nA) * nB
+    for nb in (1, 2, 3, 8):
+        bands = [skmp.mp_abband(nA, nB, dtype, nb, b) for b in range(nb)]
+        p1 = [bd[0] for bd in bands if bd[0][0] < bd[0][1]]
+        p2 = [bd[1] for bd in bands if bd[1][0] < bd[1][1]]
+        # contiguous, disjoint cover of each pass
+        assert p1[0][0] == 0 and p1[-1][1] == nB
+        assert all(a[1] == b[0] and b[0] % W == 0 for a, b in zip(p1, p1[1:]))
+        if nA > 1:
+            assert p2[0][0] == 1 and p2[-1][1] == nA
+            assert all(a[1] == b[0] and b[0] % W == 0 for a, b in zip(p2, p2[1:]))
+        else:
+            assert not p2
+        # bands are consecutive in the pass-1-then-pass-2 order
+        order = []
+        for (a1, b1), (a2, b2) in bands:
+            if a1 < b1:
+                order.append((1, a1, b1))
+            if a2 < b2:
+                order.append((2, a2, b2))
+        assert order == sorted(order)
+        tot = float(nA) * nB
+        for (a1, b1), (a2, b2) in bands:
+            got = (c1(a1, b1) if a1 < b1 else 0.0) + (c2(a2, b2) if a2 < b2 else 0.0)
+            assert abs(got - tot / nb) <= 2 * W * max(nA, nB) + 1
+
+
+def test_abband_invalid():
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_abband(0, 10, 0, 2, 0)
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_abband(10, 10, 0, 2, 2)
+
+
 def test_compute_calls_fail_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():

@@ -66,6 +66,36 @@ def _band_keys(r, m, excl, lo, hi, words):
     return keys
 
 
+def _pack(rho, j, words):
+    if words == 1:
+        v = (_ord32(float(np.float32(rho))) << 32) | (0xFFFFFFFF - int(j))
+        return [v if v < (1 << 63) else v - (1 << 64)]
+    return [_ord64(float(rho)), -1 - int(j)]
+
+
+def _ab_band_keys(a, b, m, band1, band2, words):
+    """Oracle keys of one AB band: pass 1 cells (i, j = i + delta), delta in band1 (test rows i,
+    train columns j); pass 2 cells (j, i = j + delta), delta in band2.  Returns (keys of the test
+    windows, keys of the train windows), each window's best over the cells of the band."""
+    Za, _ = ref.znorm_windows(a, m)
+    Zb, _ = ref.znorm_windows(b, m)
+    nA, nB = Za.shape[0], Zb.shape[0]
+    rho = np.empty((nA, nB))
+    for i in range(nA):
+        rho[i] = 1.0 - ((Za[i] - Zb) ** 2).sum(axis=1) / (2 * m)
+    delta = np.arange(nB)[None, :] - np.arange(nA)[:, None]        # j - i
+    cover = ((delta >= band1[0]) & (delta < band1[1])) | ((-delta >= band2[0]) & (-delta < band2[1]))
+    out = []
+    for M in (np.where(cover, rho, -np.inf), np.where(cover.T, rho.T, -np.inf)):
+        keys = np.full((M.shape[0], words), np.iinfo(np.int64).min, dtype=np.int64)
+        for i in range(M.shape[0]):
+            if np.isfinite(M[i]).any():
+                j = int(np.argmax(M[i]))            # first maximum = smallest index (reading 8)
+                keys[i] = _pack(M[i, j], j, words)
+        out.append(keys)
+    return out
+
+
 def _worker(rank, world, port, q):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -84,6 +114,17 @@ def _worker(rank, world, port, q):
             sdist.reduce_keys(k, words)
             out[f"keys{words}"] = k.numpy().reshape(n_sub, words)
             out[f"band{words}"] = (lo, hi)
+        # ---- AB-join: bands over both passes + key reduce of both sides --------------------
+        ra = synthgen.mp_series(1, 150, seed=12, kind="mix")[0]
+        rb = synthgen.mp_series(1, 260, seed=13, kind="mix")[0]
+        for dtype, words in ((skmp.F32, 1), (skmp.F64, 2)):
+            b1, b2 = skmp.mp_abband(len(ra) - m + 1, len(rb) - m + 1, dtype, world, rank)
+            ka, kb = _ab_band_keys(ra, rb, m, b1, b2, words)
+            for nm, kk in (("A", ka), ("B", kb)):
+                t = torch.from_numpy(kk.reshape(-1).copy())
+                sdist.reduce_keys(t, words)
+                out[f"ab{nm}{words}"] = t.numpy().reshape(-1, words)
+            out[f"abband{words}"] = (b1, b2)
         # ---- sketch: shard streams, sum partial sketches ---------------------------------
         cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=600, k=3)
         ids = np.arange(cfg.d)
@@ -143,6 +184,25 @@ def test_two_rank_bands_and_reductions():
                 if j[i] != I[i]:  # only a tie at the key's precision is acceptable
                     d = math.sqrt(((Z[i] - Z[j[i]]) ** 2).sum())
                     assert abs(d - P[i]) <= (1e-6 if words == 1 else 1e-12) * max(P[i], 1.0), (i, j[i], I[i])
+    # AB-join: the ranks' bands cover both passes; reduced keys give Def. 6's AB profiles
+    ra = synthgen.mp_series(1, 150, seed=12, kind="mix")[0]
+    rb = synthgen.mp_series(1, 260, seed=13, kind="mix")[0]
+    Za, _ = ref.znorm_windows(ra, m)
+    Zb, _ = ref.znorm_windows(rb, m)
+    for words in (1, 2):
+        (a1, c1), (a2, c2) = res[0][f"abband{words}"]
+        (b1_, d1), (b2_, d2) = res[1][f"abband{words}"]
+        assert a1 == 0 and (c1 == b1_ or b1_ == d1) and max(c1, d1) == Zb.shape[0]
+        assert max(c2, d2) == Za.shape[0] and min(x for x in (a2, b2_) if x > 0) == 1
+        for nm, (x, y, Zx, Zy) in (("A", (ra, rb, Za, Zb)), ("B", (rb, ra, Zb, Za))):
+            Pab, Iab = ref.abjoin_brute(x, y, m)
+            for rank in range(world):
+                keys = res[rank][f"ab{nm}{words}"]
+                j = 0xFFFFFFFF - (keys[:, 0] & 0xFFFFFFFF) if words == 1 else -1 - keys[:, 1]
+                assert np.all(keys[:, 0] > np.iinfo(np.int64).min)   # every window got a candidate
+                for i in np.where(j != Iab)[0]:
+                    d = math.sqrt(((Zx[i] - Zy[j[i]]) ** 2).sum())
+                    assert abs(d - Pab[i]) <= (1e-6 if words == 1 else 1e-12) * max(Pab[i], 1.0), (nm, i, j[i])
     # sharded finalize reassembles the whole profile on rank 0; ranks' slices tile [0, n_sub)
     Pf, If, (lo0, hi0) = res[0]["fin"]
     assert np.array_equal(Pf, P) and np.array_equal(If, I)

@@ -143,3 +143,85 @@ def test_mp_abjoin_long_windows(cuda, dtype):
     A = synthgen.mp_series(1, 1800, seed=91, kind="mix")
     B = synthgen.mp_series(1, 2500, seed=92, kind="seasonal")
     _run(cuda, A, B, 300, dtype, label=f"m=300 {dtype}")
+
+
+def _combine(keys_list, words):
+    """On-device stand-in for dist.reduce_keys over band workspaces: FP32 keys max; FP64 keys
+    max on the value word, then max on the index word among the holders of that value."""
+    import torch
+    K = torch.stack([k.view(-1, words) for k in keys_list])
+    if words == 1:
+        return K.max(dim=0).values.view(-1)
+    v = K[:, :, 0].max(dim=0).values
+    idx = torch.where(K[:, :, 0] == v, K[:, :, 1], torch.full_like(K[:, :, 1], -(1 << 63))).max(dim=0).values
+    return torch.stack([v, idx], dim=1).view(-1)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("nA,nB,m,k", [(3000, 9000, 64, 3), (9000, 2500, 33, 2), (40000, 40000, 100, 1)])
+def test_staged_abjoin_band_invariance(cuda, dtype, nA, nB, m, k):
+    """The staged AB-join (mp_create_ab / mp_join_ab / mp_finalize_ab) split into 1, 2, 3 and 5
+    mp_abband bands, keys combined like the multi-GPU reduce: keys bit-identical to the
+    one-band join and profiles identical to mp_abjoin (SURVEY §8(e) applied to f1)."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    RA = torch.from_numpy(synthgen.mp_series(k, nA, seed=21, kind="mix")).to(cuda, tdt)
+    RB = torch.from_numpy(synthgen.mp_series(k, nB, seed=22, kind="mix")).to(cuda, tdt)
+    PA0, IA0, PB0, IB0, inert0 = skmp.mp_abjoin(RA, RB, m, both=True)
+    ref_keys = None
+    for nb in (1, 2, 3, 5):
+        parts = []
+        for band in range(nb):
+            a, b = skmp.mp_create_ab(RA, m), skmp.mp_create_ab(RB, m)
+            (l1, h1), (l2, h2) = skmp.mp_abband(a.n_sub, b.n_sub, a.dtype, nb, band)
+            if l1 < h1:
+                skmp.mp_join_ab(a, b, l1, h1)
+            if l2 < h2:
+                skmp.mp_join_ab(b, a, l2, h2)
+            parts.append((a, b))
+        words = skmp.mp_keys(parts[0][0])[1]
+        ka = _combine([skmp.mp_keys(a)[0] for a, _ in parts], words)
+        kb = _combine([skmp.mp_keys(b)[0] for _, b in parts], words)
+        if ref_keys is None:
+            ref_keys = (ka.clone(), kb.clone())
+        assert torch.equal(ka, ref_keys[0]) and torch.equal(kb, ref_keys[1]), f"{nb} bands: keys differ"
+        a, b = parts[0]
+        skmp.mp_keys(a)[0].copy_(ka)
+        skmp.mp_keys(b)[0].copy_(kb)
+        # sharded finalize: row slices into zero-filled profiles, summed (the dist path)
+        PA = torch.zeros_like(PA0)
+        IA = torch.zeros_like(IA0)
+        edges = np.linspace(0, a.n_sub, nb + 1).astype(np.int64)
+        for r in range(nb):
+            if edges[r + 1] > edges[r]:
+                p, i, inert = skmp.mp_finalize_ab(a, b, int(edges[r]), int(edges[r + 1]))
+                PA += p
+                IA += i
+        PB, IB, _ = skmp.mp_finalize_ab(b, a)
+        torch.cuda.synchronize()
+        assert torch.equal(PA, PA0) and torch.equal(IA, IA0) and torch.equal(PB, PB0) and torch.equal(IB, IB0)
+        assert np.array_equal(inert, inert0)
+        for a, b in parts:
+            a.free()
+            b.free()
+
+
+def test_staged_abjoin_rejects_mixed_workspaces(cuda):
+    import torch
+    import paper_2311_03393_b200 as skmp
+    R = torch.from_numpy(synthgen.mp_series(2, 500, seed=3, kind="mix")).to(cuda, torch.float32)
+    a, b = skmp.mp_create_ab(R, 32), skmp.mp_create_ab(R[:, :400].contiguous(), 32)
+    s = skmp.mp_create(R, 32)
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_join(a)                       # AB workspace through the self-join entry
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_finalize(a)
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_join_ab(a, s, 0, 10)          # self-join workspace through the AB entry
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_join_ab(a, skmp.mp_create_ab(R.double(), 32), 0, 10)   # dtype differs
+    with pytest.raises(skmp.SkmpError):
+        skmp.mp_finalize_ab(a, b, 5, 3)
+    for w in (a, b, s):
+        w.free()
