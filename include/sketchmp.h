@@ -260,6 +260,38 @@ skmp_status mp_abband(int64_t n_subA, int64_t n_subB, int32_t dtype, int32_t nba
                       int64_t* lo1, int64_t* hi1, int64_t* lo2, int64_t* hi2);
 
 /* ---------------------------------------------------------------------------------------------
+ * Streaming test data ("lines 4-5 in Alg. 1 ... only invoke whenever
+ * a new test data is received" and a streaming matrix profile in Alg. 2).  A stream holds the
+ * train sketch's plan and statistics, a private copy of the train sketch series (prepared once
+ * as an AB workspace) and a growing test sketch of `capacity` samples per group.
+ *
+ *  stream_create  train: a built sketch (count sketch or dense; it may be modified or freed
+ *                 afterwards: everything needed is copied); cfg: m (excl ignored: AB-join),
+ *                 reseed_rows; capacity: the maximum number of test samples (m <= capacity <
+ *                 2^31).  Allocates k x capacity test sketch (FP64 master + dtype copy), profile
+ *                 P (dtype) and I (int64), all with row stride `capacity`.
+ *  stream_push    T: d x n_new [host or dev] new time points of every stream of the train plan,
+ *                 rows in the plan's order (as sketch_plan lists them), row stride ld >= n_new,
+ *                 the train sketch's dtype.  Projects them into test-sketch columns
+ *                 [n_test, n_test + n_new) with the TRAIN statistics mu_j, sigma_j (reading 25),
+ *                 then AB-joins every test window completed by them (windows [max(0, n_test-m+1),
+ *                 n_test+n_new-m+1)) against all train windows (Def. 6) and writes
+ *                 their P / I.  Enqueued on `stream`; it synchronises once (window flags D2H).
+ *  stream_view    device pointers of the test sketch R (k x capacity), P and I (k x capacity;
+ *                 columns [0, n_sub) valid), the counts, the row stride, and [host] inert flags
+ *                 per group (train series all flat and every test window so far flat) or NULL.
+ *                 Pass P, I, n_sub, ld and inert to discord_topk for Alg. 2's ranking.
+ * Errors: INVALID_ARG (NULL, capacity exceeded, bad sizes), SERIES_TOO_SHORT (train n < m), CUDA,
+ * OOM.  A failed push leaves n_test unchanged only if it fails before the projection. */
+typedef struct skmp_stream skmp_stream;
+skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int64_t capacity, void* stream,
+                          skmp_stream** out);
+skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld, void* stream);
+skmp_status stream_view(const skmp_stream* h, void** R, void** P, int64_t** I, int64_t* n_test, int64_t* n_sub,
+                        int64_t* ld, uint8_t* inert);
+void stream_free(skmp_stream* h);
+
+/* ---------------------------------------------------------------------------------------------
  * Discord detection over the sketch profiles: Alg. 2 Time-Detection + ordered
  * top-K list (reading 12):
  *   C[i] = max_{g not inert} P_g[i], G[i] = smallest maximising g (Alg. 2 strict '>' P:L262);

@@ -306,6 +306,20 @@ def refine(r: np.ndarray, m: int, excl: int | None = None):
 # the test series' windows against the training series' windows
 # ------------------------------------------------------------------------------------------
 
+def streaming_ab(T_train: np.ndarray, T_test: np.ndarray, k: int, groups, signs, m: int, S=None):
+    """f4: Alg. 2 on test data that arrives over time.  The streaming method sketches
+    each new test point with Alg. 1 lines 4-5 using the TRAIN statistics (reading 25: the test
+    series' own statistics are unknown while it streams) and joins each completed test window
+    against every train window (Def. 6 ab-join).  Its result does not depend on how
+    the points arrive, so the oracle is the batch definition: R_train = Alg. 1 on T_train,
+    R_test = Alg. 1 on T_test with the train (mu, sigma), then the brute-force AB profile per
+    group.  Returns (R_test, P, I) with P, I of shape k x (n_test - m + 1)."""
+    R_tr, mu, sigma = sketch(T_train, k, groups, signs, S)
+    R_te, _, _ = sketch(T_test, k, groups, signs, S, stats=(mu, sigma))
+    PI = [abjoin_brute(R_te[q], R_tr[q], m) for q in range(k)]
+    return R_te, np.stack([p for p, _ in PI]), np.stack([i for _, i in PI])
+
+
 def abjoin_brute(a: np.ndarray, b: np.ndarray, m: int, rows=None):
     """P[i] = min_j ||z(A_i) - z(B_j)||_2 over ALL windows j of B (no exclusion zone: the two
     series are different, Def. 6), I[i] = the smallest argmin (reading 8); flat windows per

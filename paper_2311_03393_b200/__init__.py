@@ -95,6 +95,11 @@ _SIGS = {
     "mp_finalize_ab": (ctypes.c_int, [_P, _P, _I64, _I64, _P, _P, _P, _P]),
     "mp_abband": (ctypes.c_int, [_I64, _I64, _I32, _I32, _I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                  ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "stream_create": (ctypes.c_int, [_P, ctypes.POINTER(MpCfg), _I64, _P, ctypes.POINTER(_P)]),
+    "stream_push": (ctypes.c_int, [_P, _P, _I64, _I64, _P]),
+    "stream_view": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                   ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P]),
+    "stream_free": (None, [_P]),
     "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
 }
 
@@ -488,6 +493,54 @@ def mp_abjoin(RA, RB, m: int, *, reseed_rows: int = 0, both: bool = False, strea
     if both:
         return PA, IA, PB, IB, inert.astype(bool)
     return PA, IA, inert.astype(bool)
+
+
+class Stream:
+    """Streaming test data (f4): new time points are sketched with the train plan and
+    statistics and every completed test window is AB-joined against the train sketch."""
+
+    def __init__(self, train: Sketch, m: int, capacity: int, *, reseed_rows: int = 0, stream=None):
+        cfg = _mpcfg(m, -1, reseed_rows)
+        h = ctypes.c_void_p()
+        _check(lib().stream_create(train.handle, ctypes.byref(cfg), capacity, _stream(stream), ctypes.byref(h)))
+        _, k, _, _, dt = sketch_view(train)
+        self.handle, self.m, self.k, self.cap, self.dtype = h, m, k, capacity, dt
+
+    def push(self, T, stream=None):
+        """T: d x n_new (torch CUDA tensor or numpy array, train dtype), rows in the plan order."""
+        n_new = T.shape[1]
+        ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+        _check(lib().stream_push(self.handle, _ptr(T), n_new, ld, _stream(stream)))
+
+    def view(self):
+        """(R k x n_test, P k x n_sub, I k x n_sub, inert) — zero-copy views of library memory
+        (valid until the next push or free)."""
+        import torch
+        R, P, I = _P(), _P(), _P()
+        nt, ns, ld = _I64(), _I64(), _I64()
+        inert = np.zeros(self.k, dtype=np.uint8)
+        _check(lib().stream_view(self.handle, ctypes.byref(R), ctypes.byref(P), ctypes.byref(I), ctypes.byref(nt),
+                                 ctypes.byref(ns), ctypes.byref(ld), _ptr(inert)))
+        Rt = _as_tensor(R.value, (self.k, ld.value), self.dtype)[:, :nt.value]
+        Pt = _as_tensor(P.value, (self.k, ld.value), self.dtype)[:, :ns.value]
+        It = torch.as_tensor(_DevArray(I.value, (self.k, ld.value), "<i8"), device="cuda")[:, :ns.value]
+        return Rt, Pt, It, inert.astype(bool)
+
+    def topk(self, top: int, radius: int = -1, stream=None) -> list[Discord]:
+        """Alg. 2's ordered discord list over the test windows seen so far."""
+        _, P, I, inert = self.view()
+        return discord_topk(P, I, inert, self.m, top, radius, stream)
+
+    def free(self):
+        if self.handle:
+            lib().stream_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def discord_topk(P, I, inert, m: int, top: int, radius: int = -1, stream=None) -> list[Discord]:

@@ -188,11 +188,13 @@ struct skmp_sketch {
 
 namespace {
 
-// project rows [0, rows) of Tdev into the handle with mode 0/+1/-1
-skmp_status project_rows(skmp_sketch* h, const void* Tdev, int64_t ld, int64_t rows,
+// project rows [0, rows) of Tdev (ncols samples each) into R64 / R (row stride ldr) with the
+// handle's projection kind, mode 0/+1/-1
+skmp_status project_into(const skmp_sketch* h, const void* Tdev, int64_t ld, int64_t rows, int64_t ncols,
                          const std::vector<int32_t>& gg, const std::vector<int8_t>& ss,
                          const std::vector<double>& Scols, const std::vector<double>& mu,
-                         const std::vector<double>& sigma, int mode, Temps& tmp) {
+                         const std::vector<double>& sigma, int mode, double* R64, void* R, int64_t ldr,
+                         Temps& tmp) {
   std::vector<double> inv((size_t)rows);
   for (int64_t j = 0; j < rows; ++j) inv[(size_t)j] = 1.0 / sigma[(size_t)j];
   if (h->proj == SKMP_PROJ_COUNT_SKETCH) {
@@ -225,7 +227,7 @@ skmp_status project_rows(skmp_sketch* h, const void* Tdev, int64_t ld, int64_t r
     p.mu = d_mu;
     p.inv = d_inv;
     p.sign = d_sg;
-    SKMP_CUDA(launch_project_count(Tdev, ld, h->n, h->dtype, h->k, p, mode, h->R64, h->R, tmp.st));
+    SKMP_CUDA(launch_project_count(Tdev, ld, ncols, h->dtype, h->k, p, mode, R64, R, ldr, tmp.st));
   } else {
     // dense S as k x rows row-major for the kernel
     std::vector<double> S((size_t)h->k * (size_t)rows);
@@ -236,10 +238,18 @@ skmp_status project_rows(skmp_sketch* h, const void* Tdev, int64_t ld, int64_t r
     if ((s = upload(S, &d_S, tmp)) != SKMP_OK) return s;
     if ((s = upload(mu, &d_mu, tmp)) != SKMP_OK) return s;
     if ((s = upload(inv, &d_inv, tmp)) != SKMP_OK) return s;
-    SKMP_CUDA(launch_project_dense(Tdev, ld, h->n, h->dtype, h->k, rows, d_S, rows, d_mu, d_inv,
-                                   mode, h->R64, h->R, tmp.st));
+    SKMP_CUDA(launch_project_dense(Tdev, ld, ncols, h->dtype, h->k, rows, d_S, rows, d_mu, d_inv,
+                                   mode, R64, R, ldr, tmp.st));
   }
   return SKMP_OK;
+}
+
+// project rows [0, rows) of Tdev into the handle's own sketch with mode 0/+1/-1
+skmp_status project_rows(skmp_sketch* h, const void* Tdev, int64_t ld, int64_t rows,
+                         const std::vector<int32_t>& gg, const std::vector<int8_t>& ss,
+                         const std::vector<double>& Scols, const std::vector<double>& mu,
+                         const std::vector<double>& sigma, int mode, Temps& tmp) {
+  return project_into(h, Tdev, ld, rows, h->n, gg, ss, Scols, mu, sigma, mode, h->R64, h->R, h->n, tmp);
 }
 
 }  // namespace
@@ -948,6 +958,159 @@ skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, i
   mp_free(a);
   mp_free(b);
   return s == SKMP_OK ? ok() : s;
+}
+
+// ============================================================================================
+// streaming test data (f4)
+// ============================================================================================
+}  // extern "C"
+
+struct skmp_stream {
+  skmp_sketch plan;            // the train sketch's plan and statistics; R64 / R = the test sketch (k x cap)
+  skmp_mp* train = nullptr;    // AB workspace of a private copy of the train sketch
+  void* Rtrain = nullptr;      // that copy (k x n_train, dtype)
+  void* P = nullptr;           // k x cap test profile (row stride cap)
+  int64_t* I = nullptr;
+  int64_t cap = 0, n_test = 0;
+  skmp_mp_cfg cfg{};
+  std::vector<int64_t> nflat;  // flat test windows so far, per group
+};
+
+extern "C" {
+
+skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int64_t capacity, void* stream,
+                          skmp_stream** out) {
+  if (!train || !cfg || !out) return set_error(SKMP_E_INVALID_ARG, "stream_create: NULL argument");
+  if (capacity < cfg->m || capacity >= (int64_t)INT32_MAX)
+    return set_error(SKMP_E_INVALID_ARG, "stream_create: need m <= capacity < 2^31");
+  int ex = 0;
+  skmp_status s = mp_validate(train->R, train->k, train->n, train->n, train->dtype, cfg, &ex, true);
+  if (s) return s;
+  if ((s = require_device()) != SKMP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  skmp_stream* h = new skmp_stream();
+  skmp_sketch& q = h->plan;
+  q.dtype = train->dtype;
+  q.proj = train->proj;
+  q.k = train->k;
+  q.n = capacity;
+  q.seed = train->seed;
+  q.st = st;
+  q.ids = train->ids;
+  q.g = train->g;
+  q.s = train->s;
+  q.mu = train->mu;
+  q.sigma = train->sigma;
+  q.Scol = train->Scol;
+  h->cap = capacity;
+  h->cfg = *cfg;
+  h->nflat.assign((size_t)train->k, 0);
+  const size_t es = elem_size(train->dtype), kc = (size_t)train->k * (size_t)capacity;
+  cudaError_t e = cudaMallocAsync((void**)&q.R64, sizeof(double) * kc, st);
+  if (e == cudaSuccess) {
+    if (q.dtype == SKMP_F32) e = cudaMallocAsync(&q.R, sizeof(float) * kc, st);
+    else q.R = q.R64;
+  }
+  if (e == cudaSuccess) e = cudaMallocAsync(&h->P, es * kc, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->I, sizeof(int64_t) * kc, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&h->Rtrain, es * (size_t)train->k * (size_t)train->n, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->Rtrain, train->R, es * (size_t)train->k * (size_t)train->n, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) {
+    stream_free(h);
+    return cuda_error(e, "stream_create: allocate");
+  }
+  if ((s = mp_create_impl(h->Rtrain, train->k, train->n, train->n, train->dtype, cfg, stream, &h->train, true)) !=
+      SKMP_OK) {
+    stream_free(h);
+    return s;
+  }
+  *out = h;
+  return ok();
+}
+
+skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld, void* stream) {
+  if (!h || !T) return set_error(SKMP_E_INVALID_ARG, "stream_push: NULL argument");
+  if (n_new < 1 || ld < n_new) return set_error(SKMP_E_INVALID_ARG, "stream_push: need n_new >= 1, ld >= n_new");
+  if (h->n_test + n_new > h->cap) return set_error(SKMP_E_INVALID_ARG, "stream_push: capacity exceeded");
+  skmp_status s = require_device();
+  if (s) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  skmp_sketch& q = h->plan;
+  const int64_t d = (int64_t)q.ids.size();
+  const size_t es = elem_size(q.dtype);
+  {
+    // Alg. 1 lines 4-5 for the new time points only, with the train statistics (reading 25)
+    Temps tmp(st);
+    const void* Tdev;
+    int64_t ldd;
+    if ((s = stage_input(T, d, n_new, ld, q.dtype, tmp, &Tdev, &ldd)) != SKMP_OK) return s;
+    char* Rc = static_cast<char*>(q.R) + (size_t)h->n_test * es;
+    if ((s = project_into(&q, Tdev, ldd, d, n_new, q.g, q.s, q.Scol, q.mu, q.sigma, 0, q.R64 + h->n_test, Rc,
+                          h->cap, tmp)) != SKMP_OK)
+      return s;
+  }
+  const int m = h->cfg.m;
+  const int64_t w0 = std::max<int64_t>(0, h->n_test - m + 1), w1 = h->n_test + n_new - m + 1;
+  h->n_test += n_new;
+  q.st = st;
+  if (w1 <= w0) return ok();
+  // the new test windows [w0, w1) as one series block, AB-joined against every train window
+  const int64_t B = w1 - w0;
+  skmp_mp* a = nullptr;
+  const char* blk = static_cast<const char*>(q.R) + (size_t)w0 * es;
+  if ((s = mp_create_impl(blk, q.k, B + m - 1, h->cap, q.dtype, &h->cfg, stream, &a, true)) != SKMP_OK) return s;
+  skmp_mp* tr = h->train;
+  s = join_band(a->w, tr->w, 0, tr->w.n_sub, st);
+  if (s == SKMP_OK) s = join_band(tr->w, a->w, 1, a->w.n_sub, st);
+  if (s == SKMP_OK) {
+    Temps tmp(st);
+    char* Pb = nullptr;
+    int64_t* Ib = nullptr;
+    cudaError_t e = tmp.alloc(&Pb, es * (size_t)q.k * (size_t)B);
+    if (e == cudaSuccess) e = tmp.alloc(&Ib, (size_t)q.k * (size_t)B);
+    if (e == cudaSuccess) e = launch_mp_finalize(a->w, tr->w, -1, Pb, Ib, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(static_cast<char*>(h->P) + (size_t)w0 * es, (size_t)h->cap * es, Pb, (size_t)B * es,
+                            (size_t)B * es, (size_t)q.k, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(h->I + w0, (size_t)h->cap * 8, Ib, (size_t)B * 8, (size_t)B * 8, (size_t)q.k,
+                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) s = cuda_error(e, "stream_push: finalize");
+  }
+  if (s == SKMP_OK)
+    for (int g = 0; g < q.k; ++g) h->nflat[(size_t)g] += a->nflat[(size_t)g];
+  tr->st = st;
+  mp_free(a);
+  return s == SKMP_OK ? ok() : s;
+}
+
+skmp_status stream_view(const skmp_stream* h, void** R, void** P, int64_t** I, int64_t* n_test, int64_t* n_sub,
+                        int64_t* ld, uint8_t* inert) {
+  if (!h) return set_error(SKMP_E_INVALID_ARG, "stream_view: NULL stream");
+  if (R) *R = h->plan.R;
+  if (P) *P = h->P;
+  if (I) *I = h->I;
+  const int64_t ns = std::max<int64_t>(0, h->n_test - h->cfg.m + 1);
+  if (n_test) *n_test = h->n_test;
+  if (n_sub) *n_sub = ns;
+  if (ld) *ld = h->cap;
+  if (inert)  // reading 22: inert when the train series and every test window so far are flat
+    for (int g = 0; g < h->plan.k; ++g) inert[g] = h->train->inert[(size_t)g] && h->nflat[(size_t)g] == ns;
+  return ok();
+}
+
+void stream_free(skmp_stream* h) {
+  if (!h) return;
+  cudaStream_t st = h->plan.st;
+  if (h->train) mp_free(h->train);
+  if (h->Rtrain) cudaFreeAsync(h->Rtrain, st);
+  if (h->P) cudaFreeAsync(h->P, st);
+  if (h->I) cudaFreeAsync(h->I, st);
+  if (h->plan.R && h->plan.R != h->plan.R64) cudaFreeAsync(h->plan.R, st);
+  if (h->plan.R64) cudaFreeAsync(h->plan.R64, st);
+  h->plan.R = h->plan.R64 = nullptr;
+  delete h;
 }
 
 // ============================================================================================

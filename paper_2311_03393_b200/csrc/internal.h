@@ -101,11 +101,11 @@ struct CsrPlan {
   const int8_t* sign;    // per entry
 };
 cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype, int k,
-                                 CsrPlan plan, int mode, double* R64, void* R, cudaStream_t st);
+                                 CsrPlan plan, int mode, double* R64, void* R, int64_t ldr, cudaStream_t st);
 // Dense projection: R64[g,:] (+)= sum_j S[g*ldS + j] * ((T[j,:] - mu[j]) * inv[j]).
 cudaError_t launch_project_dense(const void* T, int64_t ld, int64_t n, int dtype, int k,
                                  int64_t nstreams, const double* S, int64_t ldS, const double* mu,
-                                 const double* inv, int mode, double* R64, void* R,
+                                 const double* inv, int mode, double* R64, void* R, int64_t ldr,
                                  cudaStream_t st);
 
 // ------------------------------------------------------------------------------------------

@@ -223,7 +223,7 @@ __device__ __forceinline__ double rget(const Raw4<double>& r, int q) {
 template <typename T>
 __global__ void __launch_bounds__(kProjThreads)
 project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan plan, int mode,
-                     double* __restrict__ R64, T* __restrict__ R, bool vec) {
+                     double* __restrict__ R64, T* __restrict__ R, int64_t ldr, bool vec) {
   constexpr int U = 8;
   __shared__ int32_t s_row[kProjBatch];
   __shared__ double s_mu[kProjBatch];
@@ -234,7 +234,7 @@ project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan pl
   const int32_t e0 = plan.off[g], e1 = plan.off[g + 1];
   if (mode != 0 && e0 == e1) return;  // update of an untouched group: nothing to do
   const int64_t e = ((int64_t)blockIdx.x * kProjThreads + threadIdx.x) * 4;
-  double* r64 = R64 + (int64_t)g * n;
+  double* r64 = R64 + (int64_t)g * ldr;
   double acc[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) acc[q] = (mode != 0 && e + q < n) ? r64[e + q] : 0.0;
@@ -280,7 +280,7 @@ project_count_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, CsrPlan pl
   store_out<double>(r64, e, n, &acc[0]);
   store_out<double>(r64, e + 2, n, &acc[2]);
   if ((void*)R != (void*)R64) {
-    if constexpr (sizeof(T) == 4) store_out<float>(reinterpret_cast<float*>(R) + (int64_t)g * n, e, n, acc);
+    if constexpr (sizeof(T) == 4) store_out<float>(reinterpret_cast<float*>(R) + (int64_t)g * ldr, e, n, acc);
   }
 }
 
@@ -290,14 +290,14 @@ template <typename T>
 __global__ void project_dense_kernel(const T* __restrict__ Tm, int64_t ld, int64_t n, int k,
                                      int64_t nstreams, const double* __restrict__ S, int64_t ldS,
                                      const double* __restrict__ mu, const double* __restrict__ inv,
-                                     int mode, double* __restrict__ R64, T* __restrict__ R) {
+                                     int mode, double* __restrict__ R64, T* __restrict__ R, int64_t ldr) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int g0 = blockIdx.y * kDenseG;
   if (t >= n) return;
   double acc[kDenseG];
 #pragma unroll
   for (int q = 0; q < kDenseG; ++q)
-    acc[q] = (mode != 0 && g0 + q < k) ? R64[(int64_t)(g0 + q) * n + t] : 0.0;
+    acc[q] = (mode != 0 && g0 + q < k) ? R64[(int64_t)(g0 + q) * ldr + t] : 0.0;
   for (int64_t j = 0; j < nstreams; ++j) {
     const double z = __dmul_rn(__dsub_rn((double)Tm[j * ld + t], mu[j]), inv[j]);
 #pragma unroll
@@ -311,8 +311,8 @@ __global__ void project_dense_kernel(const T* __restrict__ Tm, int64_t ld, int64
 #pragma unroll
   for (int q = 0; q < kDenseG; ++q) {
     if (g0 + q < k) {
-      R64[(int64_t)(g0 + q) * n + t] = acc[q];
-      if ((void*)R != (void*)R64) R[(int64_t)(g0 + q) * n + t] = (T)acc[q];
+      R64[(int64_t)(g0 + q) * ldr + t] = acc[q];
+      if ((void*)R != (void*)R64) R[(int64_t)(g0 + q) * ldr + t] = (T)acc[q];
     }
   }
 }
@@ -398,19 +398,19 @@ cudaError_t launch_stream_stats(const void* T, int64_t d, int64_t n, int64_t ld,
 }
 
 cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype, int k,
-                                 CsrPlan plan, int mode, double* R64, void* R, cudaStream_t st) {
+                                 CsrPlan plan, int mode, double* R64, void* R, int64_t ldr, cudaStream_t st) {
   if (dtype == SKMP_F32) {
     const int64_t tile = (int64_t)kProjThreads * 4;
     dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
     const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 4 == 0);
     project_count_kernel<float><<<grid, kProjThreads, 0, st>>>(
-        static_cast<const float*>(T), ld, n, plan, mode, R64, static_cast<float*>(R), vec);
+        static_cast<const float*>(T), ld, n, plan, mode, R64, static_cast<float*>(R), ldr, vec);
   } else {
     const int64_t tile = (int64_t)kProjThreads * 4;
     dim3 grid((unsigned)((n + tile - 1) / tile), (unsigned)k);
     const bool vec = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ld % 2 == 0);
     project_count_kernel<double><<<grid, kProjThreads, 0, st>>>(
-        static_cast<const double*>(T), ld, n, plan, mode, R64, static_cast<double*>(R), vec);
+        static_cast<const double*>(T), ld, n, plan, mode, R64, static_cast<double*>(R), ldr, vec);
   }
   count_launches(1);
   return cudaGetLastError();
@@ -418,17 +418,17 @@ cudaError_t launch_project_count(const void* T, int64_t ld, int64_t n, int dtype
 
 cudaError_t launch_project_dense(const void* T, int64_t ld, int64_t n, int dtype, int k,
                                  int64_t nstreams, const double* S, int64_t ldS, const double* mu,
-                                 const double* inv, int mode, double* R64, void* R,
+                                 const double* inv, int mode, double* R64, void* R, int64_t ldr,
                                  cudaStream_t st) {
   dim3 grid((unsigned)((n + 255) / 256), (unsigned)((k + kDenseG - 1) / kDenseG));
   if (dtype == SKMP_F32)
     project_dense_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(T), ld, n, k,
                                                       nstreams, S, ldS, mu, inv, mode, R64,
-                                                      static_cast<float*>(R));
+                                                      static_cast<float*>(R), ldr);
   else
     project_dense_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(T), ld, n, k,
                                                        nstreams, S, ldS, mu, inv, mode, R64,
-                                                       static_cast<double*>(R));
+                                                       static_cast<double*>(R), ldr);
   count_launches(1);
   return cudaGetLastError();
 }

@@ -388,3 +388,33 @@ def test_tierb_recurrence_matches_brute_force(seed):
         Z, _ = ref.znorm_windows(r, m)
         for i in np.where(It != Ib)[0]:
             assert abs(np.sqrt(((Z[i] - Z[It[i]]) ** 2).sum()) - Pb[i]) <= 1e-10 * Pb[i]
+
+
+def test_streaming_ab_invariants():
+    """f4 oracle (reading 25) pinned by what the mathematics fixes: (1) streaming the
+    train data itself reproduces the train sketch exactly and every window finds itself (P = 0,
+    I = t); (2) with one stream the sketch is an affine map of it, which window z-normalisation
+    (Def. 3) removes, so P / I equal the raw streams' AB profile; (3) a planted test-only shape
+    is the top discord."""
+    rng = np.random.default_rng(5)
+    m = 24
+    Ttr = np.cumsum(rng.standard_normal((7, 400)), axis=1)
+    g = np.array([0, 1, 2, 0, 1, 2, 0])
+    s = np.array([1, -1, 1, 1, -1, -1, 1])
+    R_tr, _, _ = ref.sketch(Ttr, 3, g, s)
+    R_te, P, I = ref.streaming_ab(Ttr, Ttr, 3, g, s, m)
+    assert np.array_equal(R_te, R_tr)
+    assert np.all(P <= 1e-6) and np.all(I == np.arange(P.shape[1])[None, :])
+    # (2) one stream, sign -1: P equals the raw AB profile
+    x_tr = np.cumsum(rng.standard_normal(300))
+    x_te = np.cumsum(rng.standard_normal(260)) + 40.0
+    _, P1, I1 = ref.streaming_ab(x_tr[None], x_te[None], 1, [0], [-1], m)
+    Pr, Ir = ref.abjoin_brute(x_te, x_tr, m)
+    np.testing.assert_allclose(P1[0], Pr, rtol=1e-9, atol=1e-9)
+    assert np.array_equal(I1[0], Ir)
+    # (3) a sine burst only in the test data of stream 4 (group 1) is the top discord
+    Tte = Ttr[:, 50:350] + 0.01 * rng.standard_normal((7, 300))   # seen behaviour plus noise
+    Tte[4, 150:150 + m] += 6.0 * np.sin(np.linspace(0, 4 * np.pi, m))
+    _, P3, _ = ref.streaming_ab(Ttr, Tte, 3, g, s, m)
+    C, _ = ref.combine(P3, np.zeros(3, bool))
+    assert abs(int(np.argmax(C)) - 150) <= m

@@ -34,6 +34,66 @@ __device__ __forceinline__ void unpk(f2 v, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
 }
 
+__device__ __forceinline__ int imax3(int a, int b, int c) {  // ptxas fuses to VIMNMX3
+  int r;
+  asm("{ .reg .s32 t; max.s32 t, %1, %2; max.s32 %0, t, %3; }" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+__device__ __forceinline__ int itree8(const int* v) {
+  return imax3(imax3(v[0], v[1], v[2]), imax3(v[3], v[4], v[5]), imax(v[6], v[7]));
+}
+
+// scalar with integer maxima: the cell value is rho + 1 >= 0 (one FFMA instead of the last
+// FMUL), whose bit pattern orders like an int, so the row/column maxima are VIMNMX3 on the
+// ALU pipe, which (pipe_mix2.cu) overlaps with scalar FFMA
+__global__ void scalar_int_kernel(float* out, float s0, int rots) {
+  const float s = s0 + threadIdx.x * 1e-6f;
+  float cov[D], xx[D], xy[D], xz[D];
+  int CK[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    cov[d] = s * d;
+    xx[d] = s + d * 1e-3f;
+    xy[d] = s - d * 1e-3f;
+    xz[d] = s * (0.3f + 0.01f * d);
+    CK[d] = 0;
+  }
+  float ra = threadIdx.x * 1e-6f, rb = s * 0.9f, rc = s * 0.7f;
+  int sink = 0;
+  for (int it = 0; it < rots; ++it) {
+#pragma unroll
+    for (int u = 0; u < D; u += 2) {
+      int ka[D], kb[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int x = (u + d) % D;
+        cov[d] = fmaf(ra, xy[x], cov[d]);
+        cov[d] = fmaf(xx[x], rb, cov[d]);
+        ka[d] = __float_as_int(fmaf(cov[d] * xz[x], rc, 1.0f));
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        const int x = (u + 1 + d) % D;
+        cov[d] = fmaf(rb, xy[x], cov[d]);
+        cov[d] = fmaf(xx[x], ra, cov[d]);
+        kb[d] = __float_as_int(fmaf(cov[d] * xz[x], rc, 1.0f));
+      }
+      const int c0 = imax(CK[u % D], ka[0]);
+      const int c1 = imax3(CK[(u + 1) % D], ka[1], kb[0]);
+#pragma unroll
+      for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = imax3(CK[(u + d) % D], ka[d], kb[d - 1]);
+      CK[(u + D - 1) % D] = imax(ka[D - 1], kb[D - 2]);
+      CK[u % D] = kb[D - 1];
+      sink = imax3(sink, itree8(ka), itree8(kb));
+      sink = imax3(sink, c0, c1);
+      ra += 1e-7f;
+      rc += 1e-9f;
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __int_as_float(sink) + __int_as_float(CK[0]);
+}
+
 // scalar: D slots, rows in pairs, columns rotate through registers as in mp_join.cu
 __global__ void scalar_kernel(float* out, float s0, int rots) {
   const float s = s0 + threadIdx.x * 1e-6f;  // per-lane operands, as the join's column records
@@ -159,5 +219,6 @@ int main() {
   cudaMalloc(&d, 148 * 64 * 32 * 4);
   for (int w : {8, 16, 20, 32}) run(scalar_kernel, "scalar", D * D, d, w);
   for (int w : {8, 16, 20}) run(packed_kernel, "packed", 2 * D * D, d, w);
+  for (int w : {8, 16, 20, 32}) run(scalar_int_kernel, "sc-int", D * D, d, w);
   return 0;
 }
