@@ -343,13 +343,31 @@ join_x2_kernel(JoinArgs a) {
       mub[e] = (j < n_sub_c) ? muc[j] : 0.0;
       acc[e] = 0.0;
     }
-    for (int s = 0; s < a.m; ++s) {
-      const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
+    // column samples through two register rings (group A at jb, group B at jb + H): sample
+    // jb + s + d sits in slot (s + d) % DG, so each sample is loaded and converted once per
+    // thread instead of once per diagonal
+    const int64_t jb = i0 + dt;
+    double wa[DG], wb[DG];
 #pragma unroll
-      for (int e = 0; e < 2 * DG; ++e) {
-        const int64_t t = i0 + dt + (e % DG) + (e >= DG ? H : 0) + s;
-        const double bv = (t < a.nc) ? (double)Rc[t] : 0.0;
-        acc[e] = fma(av, bv - mub[e], acc[e]);
+    for (int d = 0; d < DG - 1; ++d) {
+      wa[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
+      wb[d] = (jb + H + d < a.nc) ? (double)Rc[jb + H + d] : 0.0;
+    }
+    for (int s0 = 0; s0 < a.m; s0 += DG) {
+#pragma unroll
+      for (int u = 0; u < DG; ++u) {
+        const int s = s0 + u;
+        if (s < a.m) {
+          const int64_t t = jb + s + DG - 1;
+          wa[(u + DG - 1) % DG] = (t < a.nc) ? (double)Rc[t] : 0.0;
+          wb[(u + DG - 1) % DG] = (t + H < a.nc) ? (double)Rc[t + H] : 0.0;
+          const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
+#pragma unroll
+          for (int d = 0; d < DG; ++d) {
+            acc[d] = fma(av, wa[(u + d) % DG] - mub[d], acc[d]);
+            acc[DG + d] = fma(av, wb[(u + d) % DG] - mub[DG + d], acc[DG + d]);
+          }
+        }
       }
     }
     const float4 qi = q[i0];
