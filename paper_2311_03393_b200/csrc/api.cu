@@ -111,8 +111,16 @@ skmp_status stage_input(const void* T, int64_t rows, int64_t n, int64_t ld, int 
   const size_t es = elem_size(dtype);
   char* d = nullptr;
   SKMP_CUDA(tmp.alloc(&d, (size_t)rows * (size_t)n * es));
-  SKMP_CUDA(cudaMemcpy2DAsync(d, (size_t)n * es, T, (size_t)ld * es, (size_t)n * es, (size_t)rows,
-                              cudaMemcpyHostToDevice, tmp.st));
+  // in <= 64 MB pieces: a copy engine works through one command at a time, so one multi-GB
+  // command would hold back every small transfer other streams enqueue meanwhile (e.g. a join's
+  // tile table behind the next batch's staging)
+  const int64_t piece = std::max<int64_t>(1, (int64_t)((64u << 20) / std::max<size_t>(1, (size_t)n * es)));
+  for (int64_t r0 = 0; r0 < rows; r0 += piece) {
+    const int64_t nr = std::min(piece, rows - r0);
+    SKMP_CUDA(cudaMemcpy2DAsync(d + (size_t)r0 * (size_t)n * es, (size_t)n * es,
+                                static_cast<const char*>(T) + (size_t)r0 * (size_t)ld * es, (size_t)ld * es,
+                                (size_t)n * es, (size_t)nr, cudaMemcpyHostToDevice, tmp.st));
+  }
   *dev = d;
   *dev_ld = n;
   return SKMP_OK;
