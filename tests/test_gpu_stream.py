@@ -123,3 +123,32 @@ def test_stream_self_and_errors(cuda):
     with pytest.raises(skmp.SkmpError):
         skmp.Stream(sk, m, capacity=m - 1)
     st.free()
+
+
+def test_prefetcher_overlap_results_identical(cuda):
+    """pipeline.Prefetcher: a batch sketched from pinned host memory on the prefetch stream while
+    the previous batch's join runs gives the same sketch and profile as the plain sequence."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    from paper_2311_03393_b200.pipeline import Prefetcher
+    cfg, ids, T1, T2 = _data(4000, 4000, d=30, k=4)
+    h1 = torch.from_numpy(T1.astype(np.float32)).pin_memory()
+    h2 = torch.from_numpy(T2.astype(np.float32)).pin_memory()
+    m = 50
+    stage = lambda T: skmp.sketch_build(T, ids, cfg.k, seed=cfg.seed)  # noqa: E731
+    pf = Prefetcher(cuda)
+    sk1 = pf.run(stage, h1)
+    pf.handoff()
+    w = skmp.mp_create(sk1.R, m)
+    skmp.mp_join(w)
+    sk2 = pf.run(stage, h2)             # overlaps the join above
+    P1, I1, _ = skmp.mp_finalize(w)
+    pf.handoff()
+    P2, I2, _ = skmp.mp_selfjoin(sk2.R, m)
+    torch.cuda.synchronize()
+    for T, sk, P, I in ((h1, sk1, P1, I1), (h2, sk2, P2, I2)):
+        ref_sk = skmp.sketch_build(T.to(cuda), ids, cfg.k, seed=cfg.seed)
+        assert torch.equal(ref_sk.R, sk.R)
+        Pr, Ir, _ = skmp.mp_selfjoin(ref_sk.R, m)
+        assert torch.equal(Pr, P) and torch.equal(Ir, I)
+    w.free()
