@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsketchmp.so")
 BUILD = os.path.join(ROOT, "build", "obj")
-SOURCES = ["api.cu", "hash.cpp", "sketch.cu", "mp_prep.cu", "mp_join.cu", "mp_join_x2.cu", "mp_final.cu", "detect.cu", "dims.cu"]
+SOURCES = ["api.cu", "hash.cpp", "sketch.cu", "mp_prep.cu", "mp_join.cu", "mp_join_x2.cu", "mp_final.cu", "detect.cu", "dims.cu", "stream.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

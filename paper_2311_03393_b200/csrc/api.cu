@@ -982,6 +982,12 @@ struct skmp_stream {
   int64_t cap = 0, n_test = 0;
   skmp_mp_cfg cfg{};
   std::vector<int64_t> nflat;  // flat test windows so far, per group
+  // carried AB rows (stream.cu): FP64 train records, two rings of per-diagonal covariances
+  void* q64 = nullptr;
+  double* ring[2] = {nullptr, nullptr};
+  int cur = 0;
+  bool state_valid = false;    // ring[cur] holds the covariances of test window state_t - 1
+  int64_t state_t = 0;
 };
 
 extern "C" {
@@ -1033,6 +1039,15 @@ skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int6
     stream_free(h);
     return s;
   }
+  const size_t nring = (size_t)train->k * (size_t)h->train->w.n_sub;
+  e = cudaMallocAsync(&h->q64, stream_q64_bytes(h->train->w), st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[0], sizeof(double) * nring, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[1], sizeof(double) * nring, st);
+  if (e == cudaSuccess) e = launch_train_q64(h->train->w, h->q64, st);
+  if (e != cudaSuccess) {
+    stream_free(h);
+    return cuda_error(e, "stream_create: train records");
+  }
   *out = h;
   return ok();
 }
@@ -1063,8 +1078,53 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
   h->n_test += n_new;
   q.st = st;
   if (w1 <= w0) return ok();
-  // the new test windows [w0, w1) as one series block, AB-joined against every train window
   const int64_t B = w1 - w0;
+  if (B <= kStreamIncrMax) {
+    // carried path: the block starts one window early (the predecessor row's df / dg need it)
+    const int64_t base = w0 > 0 ? w0 - 1 : 0;
+    skmp_mp* a = nullptr;
+    const char* blk = static_cast<const char*>(q.R) + (size_t)base * es;
+    if ((s = mp_create_impl(blk, q.k, w1 - 1 + m - base, h->cap, q.dtype, &h->cfg, stream, &a, true)) != SKMP_OK)
+      return s;
+    skmp_mp* tr = h->train;
+    const bool valid = h->state_valid && h->state_t == w0;
+    cudaError_t e = launch_stream_rows(a->w, base, tr->w, h->q64, h->ring[h->cur], h->ring[h->cur ^ 1], w0, (int)B,
+                                       valid, st);
+    const int64_t l0 = w0 - base, nsb = a->w.n_sub;
+    std::vector<uint8_t> pred((size_t)q.k, 0);
+    {
+      Temps tmp(st);
+      char* Pb = nullptr;
+      int64_t* Ib = nullptr;
+      if (e == cudaSuccess) e = tmp.alloc(&Pb, es * (size_t)q.k * (size_t)nsb);
+      if (e == cudaSuccess) e = tmp.alloc(&Ib, (size_t)q.k * (size_t)nsb);
+      if (e == cudaSuccess) e = launch_mp_finalize(a->w, tr->w, -1, Pb, Ib, st, l0, l0 + B);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(static_cast<char*>(h->P) + (size_t)w0 * es, (size_t)h->cap * es, Pb + (size_t)l0 * es,
+                              (size_t)nsb * es, (size_t)B * es, (size_t)q.k, cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(h->I + w0, (size_t)h->cap * 8, Ib + l0, (size_t)nsb * 8, (size_t)B * 8, (size_t)q.k,
+                              cudaMemcpyDeviceToDevice, st);
+      // the predecessor window was counted by the push that completed it
+      if (e == cudaSuccess && l0 > 0)
+        e = cudaMemcpy2DAsync(pred.data(), 1, a->w.flat, (size_t)a->w.ldq, 1, (size_t)q.k, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess && l0 > 0) e = cudaStreamSynchronize(st);
+    }
+    if (e != cudaSuccess) {
+      h->state_valid = false;
+      mp_free(a);
+      return cuda_error(e, "stream_push: carried rows");
+    }
+    for (int g = 0; g < q.k; ++g) h->nflat[(size_t)g] += a->nflat[(size_t)g] - pred[(size_t)g];
+    h->cur ^= 1;
+    h->state_valid = true;
+    h->state_t = w1;
+    tr->st = st;
+    mp_free(a);
+    return ok();
+  }
+  // the new test windows [w0, w1) as one series block, AB-joined against every train window
+  h->state_valid = false;  // the tiled join does not carry covariances
   skmp_mp* a = nullptr;
   const char* blk = static_cast<const char*>(q.R) + (size_t)w0 * es;
   if ((s = mp_create_impl(blk, q.k, B + m - 1, h->cap, q.dtype, &h->cfg, stream, &a, true)) != SKMP_OK) return s;
@@ -1113,6 +1173,9 @@ void stream_free(skmp_stream* h) {
   cudaStream_t st = h->plan.st;
   if (h->train) mp_free(h->train);
   if (h->Rtrain) cudaFreeAsync(h->Rtrain, st);
+  if (h->q64) cudaFreeAsync(h->q64, st);
+  if (h->ring[0]) cudaFreeAsync(h->ring[0], st);
+  if (h->ring[1]) cudaFreeAsync(h->ring[1], st);
   if (h->P) cudaFreeAsync(h->P, st);
   if (h->I) cudaFreeAsync(h->I, st);
   if (h->plan.R && h->plan.R != h->plan.R64) cudaFreeAsync(h->plan.R, st);

@@ -178,6 +178,15 @@ cudaError_t launch_dims(const void* X, int64_t ld, int64_t n, int dtype, const i
 void count_launches(int64_t n);
 
 // §3.3 point updates: R64[idx[q]] += coef[q] * delta[q], then R[idx] = dtype(R64[idx]) (all [dev])
+// f4 streaming (stream.cu): FP64 train records {df, dg, inv, 0} once per stream, then the AB rows
+// of each push's new test windows carried from the previous push (ring of per-diagonal covariances)
+constexpr int kStreamReseed = 8192;     // exact FP64 re-seed grid of the carried covariances (rows, 2^k)
+constexpr int kStreamIncrMax = 32;      // pushes of up to this many windows take the carried path (measured crossover)
+size_t stream_q64_bytes(const MpDev& tr);
+cudaError_t launch_train_q64(const MpDev& tr, void* q64, cudaStream_t st);
+cudaError_t launch_stream_rows(const MpDev& te, int64_t base, const MpDev& tr, const void* q64,
+                               const double* ring_in, double* ring_out, int64_t t0, int B, bool valid,
+                               cudaStream_t st);
 cudaError_t launch_point_update(double* R64, void* R, int dtype, const int64_t* idx, const double* coef,
                                 const double* delta, int64_t count, cudaStream_t st);
 
