@@ -98,9 +98,10 @@ struct Smem {
   int32_t rawtA[C], rawtB[C], rawtR[C];
 };
 
+// ring slot of column record c (0 <= c < 2^31: n_sub < 2^31, so 32-bit arithmetic suffices)
 __device__ __forceinline__ int pos(int64_t c) {
-  const int p = (int)(c % RS);
-  return (p % DG) * RSD + p / DG;
+  const uint32_t p = (uint32_t)c % (uint32_t)RS;
+  return (int)((p % DG) * RSD + p / DG);
 }
 
 // masking limits of a thread's diagonals relative to dt (3 registers instead of 2 DG)
@@ -271,16 +272,19 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 // next chunk's column record c (and c + H) and row i: raw copies + key high words (the
 // orderable rho of the current best; a possibly stale L1 copy only costs an extra publish)
+// (indices are < 2^31 + W: 32-bit offsets from the series bases)
 __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int64_t* keys, const float4* qc,
-                                           const int64_t* keysc, int64_t c, int64_t i, int64_t n_sub,
+                                           const int64_t* keysc, int64_t c64, int64_t i64, int64_t n_sub,
                                            int64_t n_sub_c, int e) {
+  const uint32_t c = (uint32_t)c64, i = (uint32_t)i64;
+  const uint32_t ns = (uint32_t)n_sub, nsc = (uint32_t)n_sub_c;
   cp_async16(&sm->rawA[e], qc + c);
-  cp_async16(&sm->rawB[e], qc + c + H);
+  cp_async16(&sm->rawB[e], qc + (c + H));
   cp_async16(&sm->rawR[e], q + i);
   const int32_t inf = 0x7f800000;  // orderable(+inf): never beaten
-  if (c < n_sub_c) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keysc + c) + 4); else sm->rawtA[e] = inf;
-  if (c + H < n_sub_c) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keysc + c + H) + 4); else sm->rawtB[e] = inf;
-  if (i < n_sub) cp_async4(&sm->rawtR[e], reinterpret_cast<const char*>(keys + i) + 4); else sm->rawtR[e] = inf;
+  if (c < nsc) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keysc + c) + 4); else sm->rawtA[e] = inf;
+  if (c + H < nsc) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keysc + (c + H)) + 4); else sm->rawtB[e] = inf;
+  if (i < ns) cp_async4(&sm->rawtR[e], reinterpret_cast<const char*>(keys + i) + 4); else sm->rawtR[e] = inf;
 }
 __device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e) {
   ColStage cs;
