@@ -61,13 +61,13 @@ __device__ __forceinline__ f2 pk(float lo, float hi) {
   return r;
 }
 __device__ __forceinline__ float lo_of(f2 v) {
-  float l, h;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
+  float l;
+  asm("{ .reg .f32 h; mov.b64 {%0, h}, %1; }" : "=f"(l) : "l"(v));
   return l;
 }
 __device__ __forceinline__ float hi_of(f2 v) {
-  float l, h;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(l), "=f"(h) : "l"(v));
+  float h;
+  asm("{ .reg .f32 l; mov.b64 {l, %0}, %1; }" : "=f"(h) : "l"(v));
   return h;
 }
 __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
