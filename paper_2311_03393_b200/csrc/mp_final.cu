@@ -104,16 +104,19 @@ __device__ __forceinline__ void fin_stage(double* xi, double* xo, const T* R, co
   constexpr int MC = FinChunk<T>::MC;
   constexpr int NI = MC / 32, NO = (MC + SPAN - 1 + 31) / 32;
   T vi[NI], vo[NO];
+  // 32-bit offsets (series lengths < 2^31) from per-row bases
+  const T* ri = R + (i + s0);
+  const int32_t ob = (int32_t)(b + s0), no = (int32_t)n_o;
 #pragma unroll
   for (int q = 0; q < NI; ++q) {
     const int s = lane + 32 * q;
-    vi[q] = s < len ? R[i + s0 + s] : (T)0;
+    vi[q] = s < len ? ri[s] : (T)0;
   }
 #pragma unroll
   for (int q = 0; q < NO; ++q) {
     const int t = lane + 32 * q;
-    int64_t idx = b + s0 + t;
-    idx = idx < 0 ? 0 : (idx >= n_o ? n_o - 1 : idx);  // only inadmissible members read clamped data
+    int32_t idx = ob + t;
+    idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);  // only inadmissible members read clamped data
     vo[q] = t < len + SPAN - 1 ? Ro[idx] : (T)0;
   }
 #pragma unroll
@@ -136,9 +139,13 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
   const int lane = threadIdx.x & 31;
   double* xi = fsm + (threadIdx.x >> 5) * fin_stride<T, SPAN>();
   double* xo = xi + MC;
-  const int64_t i = row_lo + (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  // Every lane runs the same straight-line code (no early return, the special rows' results are
+  // selected at the end): the warp shuffles then sit in convergent code, which spares the
+  // compiler's collective-convergence sequences around each of them.
+  const int64_t i_raw = row_lo + (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5);
+  const bool live = i_raw < row_hi;
+  const int64_t i = live ? i_raw : row_hi - 1;
   const int g = blockIdx.y;
-  if (i >= row_hi) return;  // warp-uniform
   const int words = (w.dtype == SKMP_F32) ? 1 : 2;
   const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
   const int64_t o = (int64_t)g * w.ldq, oo = (int64_t)g * wo.ldq;
@@ -146,12 +153,88 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
   const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
   const int m = w.m;
   const double sqm = sqrt((double)m);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll), nan = __longlong_as_double(0x7ff8000000000000ll);
   const int32_t nf = wo.nflat[g];
   const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
   const bool fi = w.flat[o + i] != 0;
-  int64_t j = -1;
-  const bool has = key_arg(keys, i, words, &j);  // j = smallest index of the winning set
+  int64_t kb = 0;
+  const bool has = key_arg(keys, i, words, &kb);  // kb = smallest index of the winning set
+  // ---- resolve the winning set [b, b + SPAN): nearest admissible member (Def. 3) --------------
+  const int64_t b = has ? kb : 0;
+  const double mi = w.mu[o + i];
+  double acc[SPAN], asum = 0.0;
+#pragma unroll
+  for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
+  for (int s0 = 0; s0 < m; s0 += MC) {
+    const int len = m - s0 < MC ? m - s0 : MC;
+    fin_stage<T, SPAN>(xi, xo, R, Ro, i, b, s0, len, wo.n, lane);
+    for (int s = lane; s < len; s += 32) {
+      const double a = xi[s] - mi;
+      asum += a;
+#pragma unroll
+      for (int d = 0; d < SPAN; ++d) acc[d] = fma(a, xo[s + d], acc[d]);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+  xsum<SPAN>(acc, lane);
+  int d = xidx<SPAN>(lane);
+  double dd = inf;  // not admissible
+  const int64_t jd = b + d;
+  if (admissible(i, jd, wo.n_sub, excl)) {
+    if (wo.flat[oo + jd]) {
+      dd = (double)m;  // reading 5: flat vs non-flat
+    } else {
+      // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i)
+      const double cov = acc[0] - wo.mu[oo + jd] * asum;
+      dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + jd]);
+    }
+  }
+#pragma unroll
+  for (int q = 16; q >= 1; q >>= 1) {  // warp argmin of (dd, d), smallest d on ties
+    const double od = __shfl_xor_sync(0xffffffffu, dd, q);
+    const int oi = __shfl_xor_sync(0xffffffffu, d, q);
+    if (od < dd || (od == dd && oi < d)) {
+      dd = od;
+      d = oi;
+    }
+  }
+  const int64_t jr = dd < inf ? b + d : -1;
+  // ---- its distance from the definition, by explicit differences (computed unconditionally
+  // on a valid window; used only when jr is a non-flat member) ---------------------------------
+  const bool exact = jr >= 0 && !wo.flat[oo + (jr >= 0 ? jr : 0)];
+  const int64_t je = exact ? jr : (b < 0 ? 0 : (b >= wo.n_sub ? wo.n_sub - 1 : b));
+  const int de = exact ? d : 0;
+  double pe;
+  {
+    const double mj = wo.mu[oo + je];
+    // z = (x - mu) * (1/sigma): one division per row instead of per element (<= 1 ulp from
+    // the textbook quotient; the oracle divides)
+    const double ii = 1.0 / w.sig64[o + i], ij = 1.0 / wo.sig64[oo + je];
+    double acc2 = 0.0;
+    if (m <= MC && exact) {  // the staged chunk still holds both windows (member d at offset d)
+      for (int s = lane; s < m; s += 32) {
+        const double zi = __dmul_rn(xi[s] - mi, ii);
+        const double zj = __dmul_rn(xo[s + de] - mj, ij);
+        const double e = zi - zj;
+        acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
+      }
+    } else {
+      for (int s = lane; s < m; s += 32) {
+        const double zi = __dmul_rn((double)R[i + s] - mi, ii);
+        const double zj = __dmul_rn((double)Ro[je + s] - mj, ij);
+        const double e = zi - zj;
+        acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
+      }
+    }
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+    pe = sqrt(acc2);
+  }
+  // ---- assemble (warp-uniform selections, no shuffles below) ----------------------------------
   double p;
+  int64_t j;
   if (fi) {
     const int64_t f = smallest_adm_flat(F, nf, i, excl);
     if (f >= 0) {
@@ -162,80 +245,11 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
       j = (excl < 0 || i - excl - 1 >= 0) ? 0 : i + excl + 1;
     }
   } else if (!has) {
-    p = __longlong_as_double(0x7ff8000000000000ll);  // no candidate (band not covered)
+    p = nan;  // no candidate (band not covered)
     j = -1;
   } else {
-    // ---- resolve the winning set [b, b + SPAN): nearest admissible member (Def. 3) ----------
-    const int64_t b = j;
-    const double mi = w.mu[o + i];
-    double acc[SPAN], asum = 0.0;
-#pragma unroll
-    for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
-    for (int s0 = 0; s0 < m; s0 += MC) {
-      const int len = m - s0 < MC ? m - s0 : MC;
-      fin_stage<T, SPAN>(xi, xo, R, Ro, i, b, s0, len, wo.n, lane);
-      for (int s = lane; s < len; s += 32) {
-        const double a = xi[s] - mi;
-        asum += a;
-#pragma unroll
-        for (int d = 0; d < SPAN; ++d) acc[d] = fma(a, xo[s + d], acc[d]);
-      }
-      __syncwarp();
-    }
-#pragma unroll
-    for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
-    xsum<SPAN>(acc, lane);
-    int d = xidx<SPAN>(lane);
-    double dd = __longlong_as_double(0x7ff0000000000000ll);  // +inf: not admissible
-    if (admissible(i, b + d, wo.n_sub, excl)) {
-      if (wo.flat[oo + b + d]) {
-        dd = (double)m;  // reading 5: flat vs non-flat
-      } else {
-        // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i)
-        const double cov = acc[0] - wo.mu[oo + b + d] * asum;
-        dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + b + d]);
-      }
-    }
-#pragma unroll
-    for (int q = 16; q >= 1; q >>= 1) {  // warp argmin of (dd, d), smallest d on ties
-      const double od = __shfl_xor_sync(0xffffffffu, dd, q);
-      const int oi = __shfl_xor_sync(0xffffffffu, d, q);
-      if (od < dd || (od == dd && oi < d)) {
-        dd = od;
-        d = oi;
-      }
-    }
-    j = dd < __longlong_as_double(0x7ff0000000000000ll) ? b + d : -1;
-    // ---- its distance from the definition, by explicit differences ---------------------------
-    if (j < 0) {
-      p = __longlong_as_double(0x7ff8000000000000ll);
-    } else if (wo.flat[oo + j]) {
-      p = sqm;
-    } else {
-      const double mj = wo.mu[oo + j];
-      // z = (x - mu) * (1/sigma): one division per row instead of per element (<= 1 ulp from
-      // the textbook quotient; the oracle divides)
-      const double ii = 1.0 / w.sig64[o + i], ij = 1.0 / wo.sig64[oo + j];
-      double acc2 = 0.0;
-      if (m <= MC) {  // the staged chunk still holds both windows (member d at offset d)
-        for (int s = lane; s < m; s += 32) {
-          const double zi = __dmul_rn(xi[s] - mi, ii);
-          const double zj = __dmul_rn(xo[s + d] - mj, ij);
-          const double e = zi - zj;
-          acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
-        }
-      } else {
-        for (int s = lane; s < m; s += 32) {
-          const double zi = __dmul_rn((double)R[i + s] - mi, ii);
-          const double zj = __dmul_rn((double)Ro[j + s] - mj, ij);
-          const double e = zi - zj;
-          acc2 = __dadd_rn(acc2, __dmul_rn(e, e));
-        }
-      }
-#pragma unroll
-      for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
-      p = sqrt(acc2);
-    }
+    j = jr;
+    p = jr < 0 ? nan : (exact ? pe : sqm);
     if (nf > 0) {
       const int64_t f = smallest_adm_flat(F, nf, i, excl);
       if (f >= 0 && (sqm < p || (sqm == p && f < j) || j < 0)) {
@@ -244,7 +258,7 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
       }
     }
   }
-  if (lane == 0) {
+  if (lane == 0 && live) {
     P[(int64_t)g * w.n_sub + i] = (T)p;
     I[(int64_t)g * w.n_sub + i] = j;
   }
