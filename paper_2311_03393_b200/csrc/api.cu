@@ -1072,6 +1072,16 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
     if ((s = project_into(&q, Tdev, ldd, d, n_new, q.g, q.s, q.Scol, q.mu, q.sigma, 0, q.R64 + h->n_test, Rc,
                           h->cap, tmp)) != SKMP_OK)
       return s;
+    // non-finite input: rejected before the columns become part of the stream (n_test unchanged)
+    int32_t* flag = nullptr;
+    int32_t hflag = INT32_MAX;
+    SKMP_CUDA(tmp.alloc(&flag, 1));
+    SKMP_CUDA(cudaMemcpyAsync(flag, &hflag, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    SKMP_CUDA(launch_nonfinite_check(q.R64, h->cap, q.k, h->n_test, n_new, flag, st));
+    SKMP_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    SKMP_CUDA(cudaStreamSynchronize(st));
+    if (hflag != INT32_MAX)
+      return set_error(SKMP_E_NONFINITE, "stream_push: non-finite value in the new points (index = its group)", hflag);
   }
   const int m = h->cfg.m;
   const int64_t w0 = std::max<int64_t>(0, h->n_test - m + 1), w1 = h->n_test + n_new - m + 1;

@@ -183,6 +183,9 @@ void count_launches(int64_t n);
 constexpr int kStreamReseed = 8192;     // exact FP64 re-seed grid of the carried covariances (rows, 2^k)
 constexpr int kStreamIncrMax = 32;      // pushes of up to this many windows take the carried path (measured crossover)
 size_t stream_q64_bytes(const MpDev& tr);
+// *flag = min(*flag, g) for every group g with a non-finite value in R64[g, col0 : col0 + ncols)
+cudaError_t launch_nonfinite_check(const double* R64, int64_t ld, int k, int64_t col0, int64_t ncols, int32_t* flag,
+                                   cudaStream_t st);
 cudaError_t launch_train_q64(const MpDev& tr, void* q64, cudaStream_t st);
 cudaError_t launch_stream_rows(const MpDev& te, int64_t base, const MpDev& tr, const void* q64,
                                const double* ring_in, double* ring_out, int64_t t0, int B, bool valid,

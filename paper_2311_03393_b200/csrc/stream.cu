@@ -178,7 +178,24 @@ stream_rows_kernel(MpDev te, int64_t base, MpDev tr, const double4* __restrict__
   }
 }
 
+// first group (+1) whose new sketch columns hold a NaN / Inf (a non-finite input propagates into
+// its group's FP64 sum: NaN stays NaN, Inf stays Inf or meets -Inf as NaN)
+__global__ void nonfinite_kernel(const double* __restrict__ R64, int64_t ld, int64_t col0, int64_t ncols,
+                                 int32_t* __restrict__ flag) {
+  const int g = blockIdx.y;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncols; t += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(R64[(int64_t)g * ld + col0 + t])) atomicMin(flag, g);
+}
+
 }  // namespace
+
+cudaError_t launch_nonfinite_check(const double* R64, int64_t ld, int k, int64_t col0, int64_t ncols, int32_t* flag,
+                                   cudaStream_t st) {
+  const unsigned bx = (unsigned)((ncols + 255) / 256 < 64 ? (ncols + 255) / 256 : 64);
+  nonfinite_kernel<<<dim3(bx, (unsigned)k), 256, 0, st>>>(R64, ld, col0, ncols, flag);
+  count_launches(1);
+  return cudaGetLastError();
+}
 
 size_t stream_q64_bytes(const MpDev& tr) { return sizeof(double4) * (size_t)tr.k * (size_t)tr.n_sub; }
 

@@ -158,6 +158,18 @@ def test_stream_self_and_errors(cuda):
     with pytest.raises(skmp.SkmpError):
         skmp.Stream(sk, m, capacity=m - 1)
     st.free()
+    # a NaN among new points is rejected and the stream stays usable
+    st = skmp.Stream(sk, m, capacity=200)
+    st.push(Td[:, :80].contiguous())
+    bad = Td[:, 80:90].clone()
+    bad[3, 4] = float("nan")
+    with pytest.raises(skmp.SkmpError) as e:
+        st.push(bad)
+    assert e.value.name == "SKMP_E_NONFINITE"
+    st.push(Td[:, 80:90].contiguous())
+    R, P, I, _ = st.view()
+    assert R.shape[1] == 90 and torch.equal(R, sk.R[:, :90]) and P.max().item() <= 1e-6 * math.sqrt(m)
+    st.free()
 
 
 def test_prefetcher_overlap_results_identical(cuda):
