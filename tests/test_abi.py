@@ -168,3 +168,19 @@ def test_abjoin_argument_validation():
     assert L.mp_abjoin(ctypes.cast(buf, ctypes.c_void_p), 10, 10, ctypes.cast(buf, ctypes.c_void_p), 100, 100, 1, 1,
                        ctypes.byref(cfg), ctypes.cast(buf, ctypes.c_void_p), ctypes.cast(i64, ctypes.c_void_p),
                        None, None, None, None) == 4
+
+
+def test_stream_and_staged_ab_null_handles():
+    """The f4 stream and staged AB-join entry points reject NULL handles / bad arguments with
+    SKMP_E_INVALID_ARG before touching a device (called through the raw ctypes symbols)."""
+    import ctypes
+    L = skmp.lib()
+    cfg = skmp._mpcfg(16)
+    out = ctypes.c_void_p()
+    assert L.stream_create(None, ctypes.byref(cfg), 100, None, ctypes.byref(out)) == 1
+    assert L.stream_push(None, None, 1, 1, None) == 1
+    assert L.stream_view(None, None, None, None, None, None, None, None) == 1
+    L.stream_free(None)                                   # no-op
+    assert L.mp_join_ab(None, None, 0, 1, None) == 1
+    assert L.mp_finalize_ab(None, None, 0, 0, None, None, None, None) == 1
+    assert L.mp_create_ab(None, 1, 100, 100, 0, ctypes.byref(cfg), None, ctypes.byref(out)) == 1
