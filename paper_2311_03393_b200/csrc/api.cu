@@ -32,6 +32,9 @@ skmp_status set_error(skmp_status s, const std::string& msg, int64_t index) {
   return s;
 }
 skmp_status cuda_error(cudaError_t e, const char* where) {
+  // clear the runtime's per-thread last error: a failed allocation is not sticky, and a stale
+  // error would otherwise surface at the next launch check of an unrelated call
+  cudaGetLastError();
   const skmp_status s = (e == cudaErrorMemoryAllocation) ? SKMP_E_OOM : SKMP_E_CUDA;
   return set_error(s, std::string(where) + ": " + cudaGetErrorString(e), -1);
 }

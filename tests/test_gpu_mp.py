@@ -168,3 +168,28 @@ def test_mp_minimal_admissible_size(cuda, dtype):
         n = 2 * excl + 2 + m - 1
         X = synthgen.mp_series(2, n, seed=100 + m, kind="noise")
         _run(cuda, X, m, dtype, label=f"minimal m={m}")
+
+
+def test_oom_is_reported_and_the_context_stays_usable(cuda):
+    """A workspace larger than the device (64 series x 2^30 windows ~ 2.8 TB) fails with
+    SKMP_E_OOM before any kernel touches the (tiny) input, and the library keeps working."""
+    import ctypes
+    import torch
+    import paper_2311_03393_b200 as skmp
+    R = torch.zeros(64, 64, device=cuda)
+    L = skmp.lib()
+    cfg = skmp._mpcfg(16)
+    h = ctypes.c_void_p()
+    n = 1 << 30
+    st = L.mp_create(skmp._ptr(R), 64, n, n, skmp.F32, ctypes.byref(cfg), skmp._stream(None), ctypes.byref(h))
+    assert st == 12, L.skmp_last_error()              # SKMP_E_OOM
+    # stream_create with an impossible capacity (64 groups x 2^30 samples ~ 1.6 TB of buffers)
+    R2 = torch.from_numpy(synthgen.mp_series(2, 3000, seed=2, kind="mix")).to(cuda, torch.float32)
+    T = torch.from_numpy(synthgen.mp_series(80, 3000, seed=3, kind="mix")).to(cuda, torch.float32)
+    skt = skmp.sketch_build(T, np.arange(80, dtype=np.uint64), 64, seed=1)
+    with pytest.raises(skmp.SkmpError) as e:
+        skmp.Stream(skt, 32, capacity=1 << 30)
+    assert e.value.name == "SKMP_E_OOM"
+    P, I, _ = skmp.mp_selfjoin(R2, 32)                 # still fine afterwards
+    torch.cuda.synchronize()
+    assert torch.isfinite(P).all()
