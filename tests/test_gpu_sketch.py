@@ -220,3 +220,20 @@ def test_point_updates(cuda, dtype, proj):
     with pytest.raises(skmp.SkmpError) as e:
         skmp.sketch_point_update(sk, [ids[0]], [cfg.n], [1.0])
     assert e.value.name == "SKMP_E_INVALID_ARG"
+
+
+def test_sketch_refresh_rerounds_the_master_copy(cuda):
+    """sketch_refresh (used after the multi-GPU sum-reduce of the FP64 master sketch) re-rounds R
+    from R64; sketch_view64 is a live view of the master."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    T = torch.from_numpy(np.random.default_rng(4).standard_normal((6, 500)).cumsum(axis=1)).to(cuda, torch.float32)
+    sk = skmp.sketch_build(T, np.arange(6, dtype=np.uint64), 3, seed=2)
+    R64 = skmp.sketch_view64(sk)
+    assert torch.equal(sk.R, R64.float())
+    R64 += 0.1234567891
+    skmp.sketch_refresh(sk)
+    torch.cuda.synchronize()
+    assert torch.equal(sk.R, R64.float())
+    skmp.sketch_free(sk)
+    assert sk.handle is None
