@@ -47,3 +47,25 @@ def test_one_rank_dist_paths(cuda, pg, dtype):
     for x, y in zip(A0[:4], A1[:4]):
         assert torch.equal(x, y)
     assert (A0[4] == A1[4]).all()
+
+
+def test_one_rank_sketch_reduce_and_alg3(cuda, pg):
+    """allreduce_sketch (NCCL sum of the FP64 master + refresh) and detect_dimension_dist (Alg. 3
+    with the maxima all-gathered) in a one-rank group equal the single-process calls."""
+    import numpy as np
+    import torch
+    import paper_2311_03393_b200 as skmp
+    from paper_2311_03393_b200 import dist as sdist
+    cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=30, n=3000, k=4)
+    T = torch.from_numpy(synthgen.streams(cfg)).to(cuda)
+    ids = synthgen.stream_ids(cfg)
+    sk = skmp.sketch_build(T, ids, cfg.k, seed=cfg.seed)
+    R0 = sk.R.clone()
+    sdist.allreduce_sketch(sk)
+    torch.cuda.synchronize()
+    assert torch.equal(sk.R, R0)
+    P, I, inert = skmp.mp_selfjoin(sk.R, cfg.m)
+    top = skmp.discord_topk(P, I, inert, m=cfg.m, top=1)
+    a = skmp.detect_dimension(sk, [(T, ids)], top[0].t, top[0].g, cfg.m)
+    b = sdist.detect_dimension_dist(sk, [(T, ids)], top[0].t, top[0].g, cfg.m, cuda)
+    assert a[0] == b[0] and abs(a[1] - b[1]) <= 1e-12 * abs(a[1]) and a[2] == b[2]
