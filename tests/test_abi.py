@@ -184,3 +184,31 @@ def test_stream_and_staged_ab_null_handles():
     assert L.mp_join_ab(None, None, 0, 1, None) == 1
     assert L.mp_finalize_ab(None, None, 0, 0, None, None, None, None) == 1
     assert L.mp_create_ab(None, 1, 100, 100, 0, ctypes.byref(cfg), None, ctypes.byref(out)) == 1
+
+
+def _c_compile(args, tmp_path):
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    return subprocess.run(["gcc", *args], capture_output=True, text=True, cwd=str(tmp_path))
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/sketchmp.h is a C header (no C++ constructs): a C99 translation unit that only
+    includes it compiles warning-free under -pedantic -Werror."""
+    src = tmp_path / "h.c"
+    src.write_text('#include "sketchmp.h"\nint main(void) { return (int)SKMP_OK; }\n')
+    r = _c_compile(["-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror",
+                    f"-I{os.path.join(ROOT, 'include')}", str(src), "-o", str(tmp_path / "h")], tmp_path)
+    assert r.returncode == 0, r.stderr
+
+
+def test_c_demo_links_against_the_library(tmp_path):
+    """examples/abi_demo.c (a plain-C user of the ABI) compiles and links against libsketchmp.so;
+    tests/test_gpu_c_abi.py runs it on a B200."""
+    r = _c_compile(["-std=c99", "-O2", os.path.join(ROOT, "examples", "abi_demo.c"),
+                    f"-I{os.path.join(ROOT, 'include')}", "-I/usr/local/cuda/include",
+                    f"-L{os.path.join(ROOT, 'paper_2311_03393_b200')}", "-lsketchmp",
+                    "-L/usr/local/cuda/lib64", "-lcudart", "-lm", "-o", str(tmp_path / "abi_demo")], tmp_path)
+    assert r.returncode == 0, r.stderr
