@@ -13,6 +13,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running (full-size configs)")
 
 
+def pytest_sessionstart(session):
+    # a fresh checkout has no libsketchmp.so (build output, git-ignored): cross-compile it once
+    # (nvcc needs no GPU); the ABI tests then load it, and -m gpu runs use the same in-tree build
+    lib = os.path.join(ROOT, "paper_2311_03393_b200", "libsketchmp.so")
+    if not os.path.exists(lib) and not os.environ.get("SKMP_LIB"):
+        from paper_2311_03393_b200 import build
+        build.build()
+
+
 @pytest.fixture(scope="session")
 def cuda():
     import torch
