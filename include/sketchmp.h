@@ -283,7 +283,7 @@ skmp_status mp_abband(int64_t n_subA, int64_t n_subB, int32_t dtype, int32_t nba
  *                 Pass P, I, n_sub, ld and inert to discord_topk for Alg. 2's ranking.
  * Errors: INVALID_ARG (NULL, capacity exceeded, bad sizes), NONFINITE (a NaN / Inf among the new
  * points; index = the first affected group; the push is discarded), SERIES_TOO_SHORT (train n < m),
- * CUDA, OOM.  A push that fails before its join leaves the stream unchanged. */
+ * CUDA, OOM.  A failed push leaves the stream as it was (n_test, profile and carried state). */
 typedef struct skmp_stream skmp_stream;
 skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int64_t capacity, void* stream,
                           skmp_stream** out);

@@ -1088,9 +1088,13 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
   }
   const int m = h->cfg.m;
   const int64_t w0 = std::max<int64_t>(0, h->n_test - m + 1), w1 = h->n_test + n_new - m + 1;
-  h->n_test += n_new;
   q.st = st;
-  if (w1 <= w0) return ok();
+  // n_test advances only when the push completes: a failed push leaves the stream as it was (its
+  // projected columns lie beyond n_test and are overwritten by the next push)
+  if (w1 <= w0) {
+    h->n_test += n_new;
+    return ok();
+  }
   const int64_t B = w1 - w0;
   if (B <= kStreamIncrMax) {
     // carried path: the block starts one window early (the predecessor row's df / dg need it)
@@ -1132,6 +1136,7 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
     h->cur ^= 1;
     h->state_valid = true;
     h->state_t = w1;
+    h->n_test += n_new;
     tr->st = st;
     mp_free(a);
     return ok();
@@ -1159,8 +1164,10 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
                             cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) s = cuda_error(e, "stream_push: finalize");
   }
-  if (s == SKMP_OK)
+  if (s == SKMP_OK) {
     for (int g = 0; g < q.k; ++g) h->nflat[(size_t)g] += a->nflat[(size_t)g];
+    h->n_test += n_new;
+  }
   tr->st = st;
   mp_free(a);
   return s == SKMP_OK ? ok() : s;
