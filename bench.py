@@ -385,6 +385,13 @@ def main():
         dim_rows = len(skmp.group_rows(gsk, int(gt.item())))
         gsk.free()
         pf = Prefetcher(dev)
+        # warm the pipelined path once (prefetch stream, its pool blocks, the handoff)
+        pending = [pf.run(stage, host_T, host_add, host_del)]
+        pf.handoff()
+        step(host_T, host_add, host_del, sk=pending.pop(0),
+             on_join=lambda: pending.append(pf.run(stage, host_T, host_add, host_del)))
+        pf.handoff()
+        pending.pop(0).free()
         barrier()
         # batches pipelined: batch s+1's H2D staging + sketch (a1-a5, on the prefetch stream,
         # issued right after batch s's join launch) overlaps that join; every batch's inputs
