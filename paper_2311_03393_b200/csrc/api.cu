@@ -11,6 +11,7 @@
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
@@ -92,9 +93,10 @@ struct Temps {
     for (void* p : ptrs) cudaFreeAsync(p, st);
   }
   template <typename T>
-  cudaError_t alloc(T** p, size_t count) {
+  cudaError_t alloc(T** p, size_t count, cudaMemPool_t pool = nullptr) {
     void* q = nullptr;
-    cudaError_t e = cudaMallocAsync(&q, count * sizeof(T) + 16, st);
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, count * sizeof(T) + 16, pool, st)
+                         : cudaMallocAsync(&q, count * sizeof(T) + 16, st);
     if (e == cudaSuccess) {
       ptrs.push_back(q);
       *p = static_cast<T*>(q);
@@ -102,6 +104,35 @@ struct Temps {
     return e;
   }
 };
+
+// Host-input staging buffers come from a pool of their own (one per device, never trimmed):
+// multi-GB staging blocks interleaved with the small workspaces of the default pool fragmented
+// it, so a later staging allocation could miss a contiguous block and grow the pool (mapping
+// gigabytes of fresh memory) in the middle of a pipelined batch.
+cudaMemPool_t staging_pool() {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if ((int)pools.size() <= dev) pools.resize((size_t)dev + 1, nullptr);
+  if (!pools[(size_t)dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;  // fall back to the default pool
+    }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[(size_t)dev] = p;
+  }
+  return pools[(size_t)dev];
+}
 
 // Stage a (possibly host) rows x ld matrix into device memory; returns the device pointer.
 skmp_status stage_input(const void* T, int64_t rows, int64_t n, int64_t ld, int dtype, Temps& tmp,
@@ -113,7 +144,7 @@ skmp_status stage_input(const void* T, int64_t rows, int64_t n, int64_t ld, int 
   }
   const size_t es = elem_size(dtype);
   char* d = nullptr;
-  SKMP_CUDA(tmp.alloc(&d, (size_t)rows * (size_t)n * es));
+  SKMP_CUDA(tmp.alloc(&d, (size_t)rows * (size_t)n * es, staging_pool()));
   // in <= 64 MB pieces: a copy engine works through one command at a time, so one multi-GB
   // command would hold back every small transfer other streams enqueue meanwhile (e.g. a join's
   // tile table behind the next batch's staging)
