@@ -1073,11 +1073,13 @@ skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int6
     stream_free(h);
     return s;
   }
+  // carried-path state: FP64 train records only for FP64 streams (FP32 streams use the train
+  // workspace's own FP32 records); rings of one value per diagonal in the stream's dtype
   const size_t nring = (size_t)train->k * (size_t)h->train->w.n_sub;
-  e = cudaMallocAsync(&h->q64, stream_q64_bytes(h->train->w), st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[0], sizeof(double) * nring, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[1], sizeof(double) * nring, st);
-  if (e == cudaSuccess) e = launch_train_q64(h->train->w, h->q64, st);
+  e = cudaMallocAsync((void**)&h->ring[0], es * nring, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[1], es * nring, st);
+  if (e == cudaSuccess && train->dtype == SKMP_F64) e = cudaMallocAsync(&h->q64, stream_q64_bytes(h->train->w), st);
+  if (e == cudaSuccess && train->dtype == SKMP_F64) e = launch_train_q64(h->train->w, h->q64, st);
   if (e != cudaSuccess) {
     stream_free(h);
     return cuda_error(e, "stream_create: train records");

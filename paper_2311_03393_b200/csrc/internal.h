@@ -181,7 +181,10 @@ void count_launches(int64_t n);
 // f4 streaming (stream.cu): FP64 train records {df, dg, inv, 0} once per stream, then the AB rows
 // of each push's new test windows carried from the previous push (ring of per-diagonal covariances)
 constexpr int kStreamReseed = 8192;     // exact FP64 re-seed grid of the carried covariances (rows, 2^k)
-constexpr int kStreamIncrMax = 32;      // pushes of up to this many windows take the carried path (measured crossover)
+#ifndef SKMP_STREAM_INCR_MAX
+#define SKMP_STREAM_INCR_MAX 32
+#endif
+constexpr int kStreamIncrMax = SKMP_STREAM_INCR_MAX;      // pushes of up to this many windows take the carried path (measured crossover)
 size_t stream_q64_bytes(const MpDev& tr);
 // *flag = min(*flag, g) for every group g with a non-finite value in R64[g, col0 : col0 + ncols)
 cudaError_t launch_nonfinite_check(const double* R64, int64_t ld, int k, int64_t col0, int64_t ncols, int32_t* flag,

@@ -178,6 +178,108 @@ stream_rows_kernel(MpDev te, int64_t base, MpDev tr, const double4* __restrict__
   }
 }
 
+// FP32 variant (FP32 sketches): the join's own arithmetic — FP32 recurrence on the train
+// workspace's FP32 records {df, dg, inv} (mp_prep.cu), exact FP64 seeds rounded to FP32, rho in
+// FP32 — with (rho, j) packed into the FP32 key word so each reduction step is one 64-bit max.
+// Carried state: one FP32 per diagonal.
+__device__ __forceinline__ long long pack_key(float rho, int64_t j) {
+  return (long long)(((uint64_t)(uint32_t)ord32(rho) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)j));
+}
+
+__global__ void __launch_bounds__(kStreamThreads)
+stream_rows_f32_kernel(MpDev te, int64_t base, MpDev tr, const float* __restrict__ ring_in,
+                       float* __restrict__ ring_out, int64_t t0, int B, bool valid, int reseed) {
+  __shared__ long long s_key[kStreamWarps][kStreamRC];
+  __shared__ float s_row[kStreamRC][3];  // df_t, dg_t, inv_t (FP32, as the join's row records)
+  const int g = blockIdx.y;
+  const int64_t N = tr.n_sub;
+  const int64_t t1 = t0 + B;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t delta0 = -(t1 - 1) + ((int64_t)blockIdx.x * kStreamThreads + threadIdx.x) * kStreamJ;
+  const int m = te.m;
+  const float* xr = static_cast<const float*>(te.R) + (int64_t)g * te.ld;
+  const float* yr = static_cast<const float*>(tr.R) + (int64_t)g * tr.ld;
+  const int64_t ot = (int64_t)g * te.ldq, oy = (int64_t)g * tr.ldq;
+  const float4* q = static_cast<const float4*>(tr.Q) + oy;  // train records {df, dg, inv, 0}
+  const float4* qt = static_cast<const float4*>(te.Q) + ot;  // test block records
+  const long long kNone = pack_key(__int_as_float(0xff800000), 0xFFFFFFFFll);  // -inf, no index
+  float cov[kStreamJ];
+  bool have[kStreamJ];
+#pragma unroll
+  for (int d = 0; d < kStreamJ; ++d) {
+    const int64_t delta = delta0 + d;
+    const int64_t jp = t0 - 1 + delta;
+    have[d] = valid && t0 > 0 && delta <= N - 1 - t0 && jp >= 0 && jp < N;
+    cov[d] = have[d] ? ring_in[(int64_t)g * N + ((delta % N) + N) % N] : 0.0f;
+  }
+  int64_t* kg = te.keys + (int64_t)g * te.n_sub;
+  float3 rec[kStreamJ];
+  auto load_rec = [&](int64_t j) -> float3 {
+    if (j < 0 || j >= N) return make_float3(0.f, 0.f, 0.f);
+    const float4 v = q[j];
+    return make_float3(v.x, v.y, v.z);
+  };
+#pragma unroll
+  for (int d = 0; d < kStreamJ - 1; ++d) rec[d] = load_rec(t0 + delta0 + d);
+  for (int64_t c0 = t0; c0 < t1; c0 += kStreamRC) {
+    const int rc = (int)(t1 - c0 < kStreamRC ? t1 - c0 : kStreamRC);
+    if (threadIdx.x < rc) {
+      const float4 v = qt[c0 + threadIdx.x - base];
+      s_row[threadIdx.x][0] = v.x;
+      s_row[threadIdx.x][1] = v.y;
+      s_row[threadIdx.x][2] = v.z;
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < rc; r0 += kStreamJ) {
+#pragma unroll
+      for (int u = 0; u < kStreamJ; ++u) {
+        const int r = r0 + u;
+        if (r >= rc) break;  // CTA-uniform
+        const int64_t t = c0 + r, l = t - base;
+        rec[(u + kStreamJ - 1) % kStreamJ] = load_rec(t + delta0 + kStreamJ - 1);
+        const float dft = s_row[r][0], dgt = s_row[r][1], invt = s_row[r][2];
+        long long best = kNone;
+#pragma unroll
+        for (int d = 0; d < kStreamJ; ++d) {
+          const int64_t j = t + delta0 + d;
+          const float3 qj = rec[(u + d) % kStreamJ];
+          if (j >= 0 && j < N) {
+            if (!have[d] || j == 0 || (t & (reseed - 1)) == 0)
+              cov[d] = (float)seed_cov<float>(xr + l, te.mu[ot + l], yr + j, tr.mu[oy + j], m);
+            else
+              cov[d] = fmaf(dft, qj.y, fmaf(qj.x, dgt, cov[d]));
+            have[d] = true;
+            best = max(best, pack_key((cov[d] * qj.z) * invt, j));
+          } else {
+            have[d] = false;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) s_key[wid][r] = best;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < rc) {
+      long long best = s_key[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < kStreamWarps; ++w) best = max(best, s_key[w][threadIdx.x]);
+      if (best != kNone) {
+        const int64_t l = c0 + threadIdx.x - base;
+        const float v = unord32((int32_t)(best >> 32));
+        const int64_t j = (int64_t)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFll));
+        if (v >= load_thr(kg, l, (float*)nullptr)) publish(kg, l, v, j);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int d = 0; d < kStreamJ; ++d) {
+    const int64_t delta = delta0 + d;
+    if (have[d] && delta <= N - 1 - (t1 - 1)) ring_out[(int64_t)g * N + ((delta % N) + N) % N] = cov[d];
+  }
+}
+
 // first group (+1) whose new sketch columns hold a NaN / Inf (a non-finite input propagates into
 // its group's FP64 sum: NaN stays NaN, Inf stays Inf or meets -Inf as NaN)
 __global__ void nonfinite_kernel(const double* __restrict__ R64, int64_t ld, int64_t col0, int64_t ncols,
@@ -217,8 +319,8 @@ cudaError_t launch_stream_rows(const MpDev& te, int64_t base, const MpDev& tr, c
   dim3 grid((unsigned)((nd + per - 1) / per), (unsigned)tr.k);
   const int reseed = kStreamReseed;
   if (te.dtype == SKMP_F32)
-    stream_rows_kernel<float><<<grid, kStreamThreads, 0, st>>>(te, base, tr, static_cast<const double4*>(q64),
-                                                               ring_in, ring_out, t0, B, valid, reseed);
+    stream_rows_f32_kernel<<<grid, kStreamThreads, 0, st>>>(te, base, tr, reinterpret_cast<const float*>(ring_in),
+                                                            reinterpret_cast<float*>(ring_out), t0, B, valid, reseed);
   else
     stream_rows_kernel<double><<<grid, kStreamThreads, 0, st>>>(te, base, tr, static_cast<const double4*>(q64),
                                                                 ring_in, ring_out, t0, B, valid, reseed);
