@@ -17,18 +17,21 @@
 namespace skmp {
 namespace {
 
-// candidate-set base of profile entry i; false if no candidate was ever published
-__device__ __forceinline__ bool key_arg(const int64_t* keys, int64_t i, int words, int64_t* base) {
+// the key word that names entry i's candidate set (FP32: the only word; FP64: the index word)
+__device__ __forceinline__ int64_t key_word(const int64_t* keys, int64_t i, int words) {
+  return words == 1 ? keys[i] : keys[2 * i + 1];
+}
+// candidate-set base from that word; false if no candidate was ever published
+__device__ __forceinline__ bool key_arg(int64_t kw, int words, int64_t* base) {
   if (words == 1) {
-    const uint32_t lo = (uint32_t)(keys[i] & 0xFFFFFFFFll);
-    const int32_t hi = (int32_t)(keys[i] >> 32);
+    const uint32_t lo = (uint32_t)(kw & 0xFFFFFFFFll);
+    const int32_t hi = (int32_t)(kw >> 32);
     if (hi == (int32_t)0x80800000 && lo == 0) return false;  // never written (init key)
     *base = (int64_t)(0xFFFFFFFFu - lo) - kKeyArgBias;
     return true;
   }
-  const int64_t w1 = keys[2 * i + 1];
-  if (w1 == INT64_MIN) return false;
-  *base = -1 - w1;
+  if (kw == INT64_MIN) return false;
+  *base = -1 - kw;
   return true;
 }
 
@@ -93,7 +96,11 @@ __device__ __forceinline__ bool admissible(int64_t i, int64_t j, int64_t n_sub_o
 // Staged values are converted to FP64 once (an FP32 -> FP64 conversion per use would cost
 // SPAN conversions per window position).
 template <typename T> struct FinChunk { static constexpr int MC = 256; };
-constexpr int kFinWarps = 8;  // rows (warps) per CTA
+constexpr int kFinWarps = 8;  // warps per CTA
+#ifndef SKMP_FIN_ROWS
+#define SKMP_FIN_ROWS 16
+#endif
+constexpr int kFinRows = SKMP_FIN_ROWS;  // consecutive rows per warp (the next row's key is loaded early)
 template <typename T, int SPAN>
 __host__ __device__ constexpr int fin_stride() { return 2 * FinChunk<T>::MC + SPAN; }  // doubles per warp
 
@@ -142,12 +149,17 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
   // Every lane runs the same straight-line code (no early return, the special rows' results are
   // selected at the end): the warp shuffles then sit in convergent code, which spares the
   // compiler's collective-convergence sequences around each of them.
-  const int64_t i_raw = row_lo + (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5);
-  const bool live = i_raw < row_hi;
-  const int64_t i = live ? i_raw : row_hi - 1;
+  const int64_t i_first = row_lo + ((int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5)) * kFinRows;
   const int g = blockIdx.y;
   const int words = (w.dtype == SKMP_F32) ? 1 : 2;
   const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
+  int64_t kw_next = key_word(keys, i_first < row_hi ? i_first : row_hi - 1, words);
+  for (int rr = 0; rr < kFinRows; ++rr) {
+  const int64_t i_raw = i_first + rr;
+  const bool live = i_raw < row_hi;
+  const int64_t i = live ? i_raw : row_hi - 1;
+  const int64_t kw = kw_next;
+  kw_next = key_word(keys, i + 1 < row_hi ? i + 1 : row_hi - 1, words);  // next row, in flight early
   const int64_t o = (int64_t)g * w.ldq, oo = (int64_t)g * wo.ldq;
   const T* R = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
   const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
@@ -158,7 +170,7 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
   const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
   const bool fi = w.flat[o + i] != 0;
   int64_t kb = 0;
-  const bool has = key_arg(keys, i, words, &kb);  // kb = smallest index of the winning set
+  const bool has = key_arg(kw, words, &kb);  // kb = smallest index of the winning set
   // ---- resolve the winning set [b, b + SPAN): nearest admissible member (Def. 3) --------------
   const int64_t b = has ? kb : 0;
   const double mi = w.mu[o + i];
@@ -262,6 +274,8 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
     P[(int64_t)g * w.n_sub + i] = (T)p;
     I[(int64_t)g * w.n_sub + i] = j;
   }
+  __syncwarp();  // the staged windows are overwritten by the next row
+  }
 }
 
 }  // namespace
@@ -270,7 +284,8 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
                                cudaStream_t st, int64_t row_lo, int64_t row_hi) {
   if (row_hi < 0) row_hi = w.n_sub;
   if (row_hi <= row_lo) return cudaSuccess;
-  dim3 grid((unsigned)((row_hi - row_lo + kFinWarps - 1) / kFinWarps), (unsigned)w.k);
+  const int64_t per = (int64_t)kFinWarps * kFinRows;
+  dim3 grid((unsigned)((row_hi - row_lo + per - 1) / per), (unsigned)w.k);
   const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
 #define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
