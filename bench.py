@@ -252,11 +252,13 @@ def main():
         f"add {0 if Tadd is None else Tadd.shape[0]}, del {0 if Tdel is None else Tdel.shape[0]}")
 
     n_sub, excl, m, k = cfg.n_sub, cfg.excl, cfg.m, cfg.k
-    lo, hi = sdist.band_for_rank(n_sub, excl, dcode, world, rank)
+    ranges = sdist.rank_diagonals(n_sub, excl, dcode, world, rank)
     cells_total = cfg.cells()
-    a0 = max(lo, excl + 1)
-    b0 = min(max(hi, a0), n_sub)
-    cells_band = k * ((b0 - a0) * n_sub - (b0 * (b0 - 1) - a0 * (a0 - 1)) // 2)
+    cells_band = 0  # cells this rank's join launches compute (incl. the shared first block)
+    for lo, hi in ranges:
+        a0 = max(lo, excl + 1)
+        b0 = min(max(hi, a0), n_sub)
+        cells_band += k * ((b0 - a0) * n_sub - (b0 * (b0 - 1) - a0 * (a0 - 1)) // 2)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     S_dense = synthgen.dense_S(cfg)[:, [int(j) for j in my_ids]] if cfg.proj == "dense" else None
@@ -288,7 +290,9 @@ def main():
         if e: e[2].record()
         w = skmp.mp_create(sk.R, m, reseed_rows=args.reseed)
         if e: e[3].record()
-        skmp.mp_join(w, lo, hi)
+        for lo, hi in ranges:
+            if hi > lo:
+                skmp.mp_join(w, lo, hi)
         if on_join is not None:  # e2e pipeline: stage the next batch while this join runs
             on_join()
         if e: e[4].record()

@@ -187,9 +187,12 @@ skmp_status mp_join(skmp_mp* w, int64_t diag_lo, int64_t diag_hi, void* stream);
  * word 1 among ties). */
 skmp_status mp_keys(skmp_mp* w, void** keys, int64_t* count, int32_t* words);
 
-/* Host-only: diagonal band `band` of `nbands` equal-cell bands of [excl+1, n_sub), edges
- * rounded to the join's tile width for dtype (so band results are bit-identical to a single
- * join).  Errors: INVALID_ARG. */
+/* Host-only: diagonal band `band` of `nbands` equal-cost bands of [excl+1, n_sub) (cost of a
+ * diagonal = its cells + 5 W for the per-tile work that does not scale with the tile height,
+ * W = mp_tile_width; the first W diagonals' cells count 4.5 times: joined while the keys are
+ * empty, they publish most), edges rounded to W (so band results are bit-identical to a single
+ * join; the first band starts at 0).  Costs measured on one B200 (tools/band_balance.py).
+ * Errors: INVALID_ARG. */
 skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, int32_t band,
                     int64_t* diag_lo, int64_t* diag_hi);
 

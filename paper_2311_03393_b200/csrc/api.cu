@@ -775,10 +775,21 @@ skmp_status mp_band(int64_t n_sub, int32_t excl, int32_t dtype, int32_t nbands, 
     *diag_lo = *diag_hi = 0;
     return ok();
   }
-  // cells of diagonals [lo0, x): S(x) = sum_{delta=lo0}^{x-1} (n_sub - delta)
+  // cost of diagonals [lo0, x): their cells, sum_{delta=lo0}^{x-1} (n_sub - delta), plus a fixed
+  // kBandDiagCost cells per diagonal for the per-tile work that does not scale with the tile's
+  // rows (exact seeds, staging prologue, the masked triangle at the end of every diagonal block):
+  // measured on one B200 (tools/band_balance.py), the short-diagonal bands of an equal-cell
+  // split ran 5-7 % longer than the others
+  const double kBandDiagCost = 5.0 * (double)W;
+  // and the first block of W diagonals is joined while every key is still empty: its rows keep
+  // improving (near neighbours), so it publishes far more than any later block (measured: the
+  // rank holding it ran ~5 ms longer at 8 bands of C4) — its cells count 4.5 times
+  const double kFirstBlockExtra = 3.5;
   auto S = [&](int64_t x) -> double {
     const double a = (double)(x - lo0);
-    return a * (double)(n_sub - lo0) - a * (a - 1.0) / 2.0;
+    const double f = (double)std::min<int64_t>(x - lo0, W);
+    return a * (double)(n_sub - lo0) - a * (a - 1.0) / 2.0 + kBandDiagCost * a +
+           kFirstBlockExtra * (f * (double)(n_sub - lo0) - f * (f - 1.0) / 2.0);
   };
   const double total = S(n_sub);
   auto edge = [&](int32_t p) -> int64_t {

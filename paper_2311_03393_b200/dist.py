@@ -3,7 +3,7 @@
 Sketch: streams are sharded over ranks; each rank builds the partial sketch of its shard with
 the shared (seeded, id-keyed) plan, and the FP64 master accumulators are sum-all-reduced
 (linearity of Alg. 1), then re-rounded on every rank (sketch_refresh).
-Join: the diagonals [excl+1, n_sub) are split into equal-cell bands on the tile grid (mp_band);
+Join: the diagonals are split into equal-cost bands on the tile grid (mp_band, rank_diagonals);
 each rank joins its band into its own profile keys, which are max-all-reduced (FP32: one signed
 int64 MAX on {orderable rho, ~j}; FP64: MAX on the value word, then MAX on the index word among
 the ranks holding that value), after which any rank can finalize.
@@ -22,7 +22,8 @@ import torch
 import torch.distributed as dist
 
 from . import (F32, F64, Sketch, detect_dimension, mp_abband, mp_band, mp_create, mp_create_ab, mp_finalize,
-               mp_finalize_ab, mp_finalize_rows, mp_join, mp_join_ab, mp_keys, sketch_refresh, sketch_view64)
+               mp_finalize_ab, mp_finalize_rows, mp_join, mp_join_ab, mp_keys, mp_tile_width, sketch_refresh,
+               sketch_view64)
 
 INT64_MIN = -(1 << 63)
 
@@ -34,6 +35,16 @@ def shard(ids, rank: int, world: int):
 
 def band_for_rank(n_sub: int, excl: int, dtype: int, world: int, rank: int) -> tuple[int, int]:
     return mp_band(n_sub, excl, dtype, world, rank)
+
+
+def rank_diagonals(n_sub: int, excl: int, dtype: int, world: int, rank: int) -> list[tuple[int, int]]:
+    """Diagonal ranges rank `rank` joins: its equal-cost band of the whole join (mp_band; one
+    rank: everything).  A variant that had every rank also join the first block (to fill all keys
+    with good thresholds first) was measured slower: that block is the most expensive one
+    (tools/band_balance.py)."""
+    if world == 1:
+        return [(0, n_sub)]
+    return [mp_band(n_sub, excl, dtype, world, rank)]
 
 
 def allreduce_sketch(sk: Sketch, group=None) -> None:
@@ -70,8 +81,9 @@ def mp_selfjoin_dist(R: torch.Tensor, m: int, *, excl: int = -1, reseed_rows: in
     e = (m + 1) // 2 if excl < 0 else excl
     dtype = F32 if R.dtype == torch.float32 else F64
     w = mp_create(R, m, excl=e, reseed_rows=reseed_rows)
-    lo, hi = band_for_rank(n_sub, e, dtype, world, rank)
-    mp_join(w, lo, hi)
+    for lo, hi in rank_diagonals(n_sub, e, dtype, world, rank):
+        if hi > lo:
+            mp_join(w, lo, hi)
     keys, words = mp_keys(w)
     reduce_keys(keys, words, group)
     out = None

@@ -67,13 +67,16 @@ def test_band_partition(n_sub, excl, dtype):
         assert edges[0][0] == 0 and edges[-1][1] == n_sub
         for (a, b_), (c, d) in zip(edges, edges[1:]):
             assert b_ == c and c % W == 0 and a <= b_
-        # balance: each band within one tile-width of cells of the ideal share
+        # balance: each band within one tile-width of diagonals of the ideal share of the cost
+        # (cells + 5 W per diagonal, the per-tile work that does not scale with rows)
         lo0 = excl + 1
-        cells = lambda a, b: sum(max(0, n_sub - x) for x in range(max(a, lo0), b)) if n_sub < 10**5 else \
-            (lambda A, B: (B - A) * n_sub - (B * (B - 1) - A * (A - 1)) // 2)(max(a, lo0), max(b, lo0))
-        tot = cells(0, n_sub)
+        def cum(x):  # cost of diagonals [lo0, x): cells + 5 W each, first W diagonals' cells x 4.5
+            A = max(x, lo0) - lo0
+            F = min(A, W)
+            return (A * (n_sub - lo0) - A * (A - 1) // 2 + 5 * W * A + 3.5 * (F * (n_sub - lo0) - F * (F - 1) // 2))
+        tot = cum(n_sub)
         for a, b in edges:
-            assert abs(cells(a, b) - tot / nb) <= W * n_sub + 1
+            assert abs((cum(b) - cum(a)) - tot / nb) <= 4.5 * W * (n_sub + 5 * W) + 1
 
 
 @pytest.mark.parametrize("nA,nB,dtype", [(199745, 199745, 0), (9901, 99873, 0), (99873, 9901, 0), (1951, 1951, 1),
@@ -212,3 +215,16 @@ def test_c_demo_links_against_the_library(tmp_path):
                     f"-L{os.path.join(ROOT, 'paper_2311_03393_b200')}", "-lsketchmp",
                     "-L/usr/local/cuda/lib64", "-lcudart", "-lm", "-o", str(tmp_path / "abi_demo")], tmp_path)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("n_sub,excl,dtype", [(199745, 128, 0), (1999745, 128, 0), (19901, 50, 1), (700, 8, 0)])
+def test_rank_diagonals_tile_the_join(n_sub, excl, dtype):
+    """dist.rank_diagonals: the ranks' bands tile [0, n_sub) contiguously on the tile grid."""
+    from paper_2311_03393_b200 import dist as sdist
+    W = skmp.mp_tile_width(dtype)
+    assert sdist.rank_diagonals(n_sub, excl, dtype, 1, 0) == [(0, n_sub)]
+    for world in (2, 4, 8):
+        bands = [sdist.rank_diagonals(n_sub, excl, dtype, world, r)[0] for r in range(world)]
+        assert bands[0][0] == 0 and bands[-1][1] == n_sub
+        for (a, b), (c, d) in zip(bands, bands[1:]):
+            assert b == c and c % W == 0 and a <= b
