@@ -296,6 +296,31 @@ skmp_status stream_view(const skmp_stream* h, void** R, void** P, int64_t** I, i
 void stream_free(skmp_stream* h);
 
 /* ---------------------------------------------------------------------------------------------
+ * Native multi-GPU: one process per GPU, an NCCL communicator, the two exchange
+ * steps of the path.  (The Python package does the same through torch.distributed, dist.py.)
+ *  skmp_comm_unique_id  rank 0 creates the 128-byte id; the caller ships it to every rank.
+ *  skmp_comm_init       collective over `nranks` processes (each on its own current device).
+ *  sketch_allreduce     NC1: sum-all-reduce of the per-rank partial FP64 sketches (each rank built
+ *                       its shard of the streams with the same id-keyed plan; Alg. 1 is linear,
+ *                       P:L330), then R = dtype(R64) on every rank.  Asynchronous on `stream`.
+ *  mp_selfjoin_dist     mp_selfjoin split over the ranks: rank r joins band r of mp_band, the
+ *                       profile keys are max-all-reduced (NC2; FP64 keys lexicographically), each
+ *                       rank finalizes a contiguous slice of the windows and a sum-all-reduce
+ *                       assembles P, I on EVERY rank (bit-identical to mp_selfjoin).  Arguments
+ *                       as mp_selfjoin; every rank must pass the same R contents and sizes.
+ * NCCL is loaded with dlopen("libnccl.so.2") on first use (a process that already holds one
+ * reuses it).  Errors: INVALID_ARG, CUDA (incl. NCCL failures and a missing libnccl), OOM and
+ * those of the composed calls.  A rank that fails returns without entering the remaining
+ * collectives: callers pass identical arguments so that all ranks fail alike. */
+typedef struct skmp_comm skmp_comm;
+skmp_status skmp_comm_unique_id(uint8_t id[128]);
+skmp_status skmp_comm_init(const uint8_t id[128], int nranks, int rank, skmp_comm** out);
+void skmp_comm_free(skmp_comm* comm);
+skmp_status sketch_allreduce(skmp_comm* comm, skmp_sketch* partial, void* stream);
+skmp_status mp_selfjoin_dist(skmp_comm* comm, const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
+                             const skmp_mp_cfg* cfg, void* P, int64_t* I, uint8_t* inert, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * Discord detection over the sketch profiles: Alg. 2 Time-Detection + ordered
  * top-K list (reading 12):
  *   C[i] = max_{g not inert} P_g[i], G[i] = smallest maximising g (Alg. 2 strict '>' P:L262);

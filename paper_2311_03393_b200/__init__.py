@@ -100,6 +100,11 @@ _SIGS = {
     "stream_view": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P),
                                    ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P]),
     "stream_free": (None, [_P]),
+    "skmp_comm_unique_id": (ctypes.c_int, [_P]),
+    "skmp_comm_init": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "skmp_comm_free": (None, [_P]),
+    "sketch_allreduce": (ctypes.c_int, [_P, _P, _P]),
+    "mp_selfjoin_dist": (ctypes.c_int, [_P, _P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
     "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
 }
 
@@ -493,6 +498,55 @@ def mp_abjoin(RA, RB, m: int, *, reseed_rows: int = 0, both: bool = False, strea
     if both:
         return PA, IA, PB, IB, inert.astype(bool)
     return PA, IA, inert.astype(bool)
+
+
+class Comm:
+    """Native NCCL communicator of the C-ABI (skmp_comm_*): one per process / GPU.  The 128-byte
+    id comes from Comm.unique_id() on rank 0 and is shipped to the other ranks by the caller."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().skmp_comm_unique_id(ctypes.cast(buf, _P)))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = _P()
+        _check(lib().skmp_comm_init(ctypes.cast(buf, _P), nranks, rank, ctypes.byref(h)))
+        self.handle, self.nranks, self.rank = h, nranks, rank
+
+    def free(self):
+        if self.handle:
+            lib().skmp_comm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sketch_allreduce(comm: Comm, sk: Sketch, stream=None):
+    """NC1 through the native communicator: sum the per-rank partial sketches, refresh R."""
+    _check(lib().sketch_allreduce(comm.handle, sk.handle, _stream(stream)))
+
+
+def mp_selfjoin_dist(comm: Comm, R, m: int, *, excl: int = -1, reseed_rows: int = 0, stream=None):
+    """mp_selfjoin split over the communicator's ranks (C-ABI mp_selfjoin_dist): every rank gets
+    the full (P, I, inert)."""
+    import torch
+    k, n = R.shape
+    dt = _dtype_code(R)
+    tdt = torch.float32 if dt == F32 else torch.float64
+    P = torch.empty((k, n - m + 1), dtype=tdt, device=R.device)
+    I = torch.empty((k, n - m + 1), dtype=torch.int64, device=R.device)
+    inert = np.zeros(k, dtype=np.uint8)
+    cfg = _mpcfg(m, excl, reseed_rows)
+    _check(lib().mp_selfjoin_dist(comm.handle, _ptr(R), k, n, R.stride(0), dt, ctypes.byref(cfg), _ptr(P), _ptr(I),
+                                  _ptr(inert), _stream(stream)))
+    return P, I, inert.astype(bool)
 
 
 class Stream:

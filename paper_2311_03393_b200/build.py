@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsketchmp.so")
 BUILD = os.path.join(ROOT, "build", "obj")
-SOURCES = ["api.cu", "hash.cpp", "sketch.cu", "mp_prep.cu", "mp_join.cu", "mp_join_x2.cu", "mp_final.cu", "detect.cu", "dims.cu", "stream.cu"]
+SOURCES = ["api.cu", "hash.cpp", "sketch.cu", "mp_prep.cu", "mp_join.cu", "mp_join_x2.cu", "mp_final.cu", "detect.cu", "dims.cu", "stream.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -57,7 +57,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
         objs = list(ex.map(lambda s: _compile(s, force, defines, objdir), SOURCES))
     if force or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
         tmp = out + f".tmp{os.getpid()}"
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-ldl"])
         os.replace(tmp, out)
     if verbose:
         print(out)

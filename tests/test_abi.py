@@ -228,3 +228,19 @@ def test_rank_diagonals_tile_the_join(n_sub, excl, dtype):
         assert bands[0][0] == 0 and bands[-1][1] == n_sub
         for (a, b), (c, d) in zip(bands, bands[1:]):
             assert b == c and c % W == 0 and a <= b
+
+
+def test_native_comm_argument_validation():
+    """skmp_comm_* / sketch_allreduce / mp_selfjoin_dist reject NULL / bad arguments before any
+    NCCL or device work."""
+    import ctypes
+    L = skmp.lib()
+    out = ctypes.c_void_p()
+    buf = (ctypes.c_uint8 * 128)()
+    assert L.skmp_comm_unique_id(None) == 1
+    assert L.skmp_comm_init(None, 1, 0, ctypes.byref(out)) == 1
+    assert L.skmp_comm_init(ctypes.cast(buf, ctypes.c_void_p), 2, 2, ctypes.byref(out)) == 1
+    assert L.sketch_allreduce(None, None, None) == 1
+    cfg = skmp._mpcfg(16)
+    assert L.mp_selfjoin_dist(None, None, 1, 100, 100, 0, ctypes.byref(cfg), None, None, None, None) == 1
+    L.skmp_comm_free(None)
