@@ -92,9 +92,9 @@ struct Smem {
   float thrA[RS];     // column thresholds of group A columns (record base c)
   float thrB[RS];     // ... of group B columns (c + H)
   float rthr[2 * C];
-  // raw next-chunk records / key high words, staged by cp.async (no registers held across the
-  // chunk) and repacked into the pair layout above when the chunk ends
-  float4 rawA[C], rawB[C], rawR[C];
+  // next-chunk key high words (orderable rho), staged by cp.async and converted to the float
+  // thresholds above when the chunk ends; the next chunk's records go straight into their ring
+  // slots (free while this chunk runs) in the pair layout, 4 bytes per cp.async
   int32_t rawtA[C], rawtB[C], rawtR[C];
 };
 
@@ -270,33 +270,46 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-// next chunk's column record c (and c + H) and row i: raw copies + key high words (the
-// orderable rho of the current best; a possibly stale L1 copy only costs an extra publish)
-// (indices are < 2^31 + W: 32-bit offsets from the series bases)
+// next chunk's column record c (and c + H) and row i: the records straight into their ring
+// slots in the pair layout ({df_c, df_c+H}, {dg_c, dg_c+H}, {inv_c, inv_c+H}; rows duplicated),
+// the key high words into the raw threshold buffers (a possibly stale L1 copy only costs an
+// extra publish).  Indices are < 2^31 + W: 32-bit offsets from the series bases.
 __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int64_t* keys, const float4* qc,
                                            const int64_t* keysc, int64_t c64, int64_t i64, int64_t n_sub,
                                            int64_t n_sub_c, int e) {
   const uint32_t c = (uint32_t)c64, i = (uint32_t)i64;
   const uint32_t ns = (uint32_t)n_sub, nsc = (uint32_t)n_sub_c;
-  cp_async16(&sm->rawA[e], qc + c);
-  cp_async16(&sm->rawB[e], qc + (c + H));
-  cp_async16(&sm->rawR[e], q + i);
+  const float* a = reinterpret_cast<const float*>(qc + c);
+  const float* b = reinterpret_cast<const float*>(qc + (c + H));
+  const int ec = pos(c64);
+  float* d0 = reinterpret_cast<float*>(&sm->col0[ec]);  // {df_A, df_B, dg_A, dg_B}
+  float* d1 = reinterpret_cast<float*>(&sm->col1[ec]);  // {inv_A, inv_B}
+  cp_async4(d0 + 0, a + 0);
+  cp_async4(d0 + 1, b + 0);
+  cp_async4(d0 + 2, a + 1);
+  cp_async4(d0 + 3, b + 1);
+  cp_async4(d1 + 0, a + 2);
+  cp_async4(d1 + 1, b + 2);
+  const float* r = reinterpret_cast<const float*>(q + i);
+  const int er = (int)(i & (2 * C - 1));
+  float* r0 = reinterpret_cast<float*>(&sm->row0[er]);  // {df, df, dg, dg}
+  float* r1 = reinterpret_cast<float*>(&sm->row1[er]);  // {inv, inv}
+  cp_async4(r0 + 0, r + 0);
+  cp_async4(r0 + 1, r + 0);
+  cp_async4(r0 + 2, r + 1);
+  cp_async4(r0 + 3, r + 1);
+  cp_async4(r1 + 0, r + 2);
+  cp_async4(r1 + 1, r + 2);
   const int32_t inf = 0x7f800000;  // orderable(+inf): never beaten
   if (c < nsc) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keysc + c) + 4); else sm->rawtA[e] = inf;
   if (c + H < nsc) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keysc + (c + H)) + 4); else sm->rawtB[e] = inf;
   if (i < ns) cp_async4(&sm->rawtR[e], reinterpret_cast<const char*>(keys + i) + 4); else sm->rawtR[e] = inf;
 }
 __device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e) {
-  ColStage cs;
-  cs.qa = sm->rawA[e];
-  cs.qb = sm->rawB[e];
-  cs.ta = unord32(sm->rawtA[e]);
-  cs.tb = unord32(sm->rawtB[e]);
-  land_col(cs, sm, c);
-  RowStage rs;
-  rs.q = sm->rawR[e];
-  rs.t = unord32(sm->rawtR[e]);
-  land_row(rs, sm, i);
+  const int ec = pos(c);
+  sm->thrA[ec] = unord32(sm->rawtA[e]);
+  sm->thrB[ec] = unord32(sm->rawtB[e]);
+  sm->rthr[(int)(i & (2 * C - 1))] = unord32(sm->rawtR[e]);
 }
 
 #ifndef SKMP_X2_MINB
