@@ -119,17 +119,23 @@ struct Col {
 // smallest index of the winning D-cell set (resolved exactly in mp_final.cu): a row's set is one
 // group's DG diagonals of this thread (group B when its maximum is strictly larger: ties go to
 // the smaller indices of group A), a column's set is the DG rows it spent in this thread.
+// GROUPS: the caller already knows whether group B holds each row's maximum (bA, bB; masked
+// rotations, which keep the two group trees); otherwise the row maxima came from one 2 DG-cell
+// tree and the winning group is B only when group A's own maximum falls short of it (ties to
+// A's smaller indices either way)
+template <bool GROUPS>
 SKMP_X2_PUB_ATTR void publish_x2(int64_t* keys, int64_t* keysc, Smem* sm, int rbu, int ctA0, int ctA1,
                                         int64_t i_u, int64_t dt, float rowa, float rowb, const float (&ka)[DG],
-                                        const float (&la)[DG], float cA0, float cA1, float cB0, float cB1) {
-  // the row maxima came from one 2 DG-cell tree; the winning group is B only when group A's own
-  // maximum falls short of it (ties to A's smaller indices, as before)
+                                        const float (&la)[DG], bool bA, bool bB, float cA0, float cA1, float cB0,
+                                        float cB1) {
   if (rowa >= sm->rthr[rbu]) {
-    publish(keys, i_u, rowa, i_u + dt + (tree_max<float, DG>(ka) < rowa ? H : 0));
+    const bool b = GROUPS ? bA : tree_max<float, DG>(ka) < rowa;
+    publish(keys, i_u, rowa, i_u + dt + (b ? H : 0));
     sm->rthr[rbu] = rowa;
   }
   if (rowb >= sm->rthr[rbu + 1]) {
-    publish(keys, i_u + 1, rowb, i_u + 1 + dt + (tree_max<float, DG>(la) < rowb ? H : 0));
+    const bool b = GROUPS ? bB : tree_max<float, DG>(la) < rowb;
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt + (b ? H : 0));
     sm->rthr[rbu + 1] = rowb;
   }
   // columns c = i + dt (A) and c + H (B) complete after row i: their rows are [i - DG + 1, i]
@@ -216,24 +222,37 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (
     CA[u % DG] = la[DG - 1];
     CB[u % DG] = lb[DG - 1];
     // -- row maxima per group --
-    // -- row maxima: one tree over both groups' 2 DG cells (one instruction fewer per row than
-    // two group trees and their max) --
-    float kab[2 * DG], lab[2 * DG];
+    // -- row maxima: unmasked rotations use one tree over both groups' 2 DG cells (one
+    // instruction fewer per row than two group trees and their max); masked rotations keep the
+    // group trees (fewer live registers where the masks already need them) --
+    float rowa, rowb;
+    bool bA = false, bB = false;
+    if (MASKED) {
+      const float rowaA = tree_max<float, DG>(ka), rowaB = tree_max<float, DG>(kb);
+      const float rowbA = tree_max<float, DG>(la), rowbB = tree_max<float, DG>(lb);
+      rowa = max2(rowaA, rowaB);
+      rowb = max2(rowbA, rowbB);
+      bA = rowaB > rowaA;
+      bB = rowbB > rowbA;
+    } else {
+      float kab[2 * DG], lab[2 * DG];
 #pragma unroll
-    for (int d = 0; d < DG; ++d) {
-      kab[d] = ka[d];
-      kab[DG + d] = kb[d];
-      lab[d] = la[d];
-      lab[DG + d] = lb[d];
+      for (int d = 0; d < DG; ++d) {
+        kab[d] = ka[d];
+        kab[DG + d] = kb[d];
+        lab[d] = la[d];
+        lab[DG + d] = lb[d];
+      }
+      rowa = tree_max<float, 2 * DG>(kab);
+      rowb = tree_max<float, 2 * DG>(lab);
     }
-    const float rowa = tree_max<float, 2 * DG>(kab), rowb = tree_max<float, 2 * DG>(lab);
     // -- check-then-publish (rare) --
     const int t0 = (u % DG) * RSD + qt, t1 = ((u + 1) % DG) * RSD + qt;
     // ">=": exact ties always reach the atomic (keys independent of tile order / band split)
     const bool hit = (rowa >= sm->rthr[rb + u]) | (rowb >= sm->rthr[rb + u + 1]) | (cA0 >= sm->thrA[t0]) |
                      (cA1 >= sm->thrA[t1]) | (cB0 >= sm->thrB[t0]) | (cB1 >= sm->thrB[t1]);
     if (__any_sync(0xffffffffu, hit))
-      publish_x2(keys, keysc, sm, rb + u, t0, t1, ib + u, dt, rowa, rowb, ka, la, cA0, cA1, cB0, cB1);
+      publish_x2<MASKED>(keys, keysc, sm, rb + u, t0, t1, ib + u, dt, rowa, rowb, ka, la, bA, bB, cA0, cA1, cB0, cB1);
   }
 }
 
