@@ -194,8 +194,7 @@ __device__ __forceinline__ void load_col(Col& x, const Smem* sm, int e) {
 template <bool MASKED>
 __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (&CA)[DG], float (&CB)[DG],
                                             Smem* sm, int rb, int qt, int qt1, int64_t ib, int64_t dt,
-                                            const Lim& lim,
-                                            int64_t* keys, int64_t* keysc) {
+                                            const Lim& lim, const JoinArgs& a, int g) {
 #pragma unroll
   for (int u = 0; u < DG; u += 2) {
     // -- row u: its entering column (slot DG-1) takes the register of the column completed at u-1
@@ -251,8 +250,13 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], float (
     // ">=": exact ties always reach the atomic (keys independent of tile order / band split)
     const bool hit = (rowa >= sm->rthr[rb + u]) | (rowb >= sm->rthr[rb + u + 1]) | (cA0 >= sm->thrA[t0]) |
                      (cA1 >= sm->thrA[t1]) | (cB0 >= sm->thrB[t0]) | (cB1 >= sm->thrB[t1]);
-    if (__any_sync(0xffffffffu, hit))
+    if (__any_sync(0xffffffffu, hit)) {
+      // the key pointers are rebuilt from the kernel parameters here (rare path) instead of
+      // occupying registers across the hot loop
+      int64_t* keys = a.keys + (int64_t)g * a.n_sub;
+      int64_t* keysc = a.keysc + (int64_t)g * a.n_sub_c;
       publish_x2<MASKED>(keys, keysc, sm, rb + u, t0, t1, ib + u, dt, rowa, rowb, ka, la, bA, bB, cA0, cA1, cB0, cB1);
+    }
   }
 }
 
@@ -463,9 +467,9 @@ join_x2_kernel(JoinArgs a) {
     for (int it = 0; it < nrot; ++it, ib += DG) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys, keysc);
+        rotation_x2<true>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, a, g);
       else
-        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, keys, keysc);
+        rotation_x2<false>(cov, X, CA, CB, &sm, rb, qt, qt1, ib, dt, lim, a, g);
       qt = qt1;
       rb = (rb + DG) & (2 * C - 1);
     }
