@@ -44,7 +44,7 @@ import numpy as np  # noqa: E402
 METRIC = "MP cell updates/s (k·n²/2) at 1/2/4/8 B200; sketch HBM GB/s"
 UNIT = "cell updates/s"
 FP32_PIPE_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # B200: 148 SMs x 128 FP32 lanes x FMA x max clock
-FLOPS_PER_CELL = 6                                    # 2 FFMA (4 flop) + 2 FMUL (2 flop), DESIGN.md §6
+FLOPS_PER_CELL = 6                                    # 2 FFMA (4 flop) + 2 FMUL (2 flop), DESIGN.md §5
 FP64_PIPE_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
@@ -481,7 +481,7 @@ def main():
                      "kernel": join_kernel_name(cfg.dtype),
                      "note": f"{FLOPS_PER_CELL} algorithmic FLOP per cell x cells of this rank's band / mean "
                              f"mp_join event time; peak = 148 SM x {128 if cfg.dtype == 'f32' else 64} lanes x 2 x "
-                             f"1.965 GHz (derived, DESIGN.md §6)",
+                             f"1.965 GHz (derived, DESIGN.md §5)",
                      "pipe_frac": (cells_band / (phase['mp_join_ms'] / 1e3)) * 4 /
                                   (148 * (128 if cfg.dtype == 'f32' else 64) * 1.965e9)},
         "sketch": {"bound": "hbm", "achieved": sk_gbs, "peak": hbm_peak, "unit": "GB/s",
