@@ -24,6 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-diag-suppress", "177"]
+# extra nvcc flags for experiments (variant builds), e.g. SKMP_NVCC_EXTRA="-Xptxas --allow-expensive-optimizations=true"
+FLAGS += os.environ.get("SKMP_NVCC_EXTRA", "").split()
 
 
 def _deps_mtime() -> float:
