@@ -3,9 +3,11 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
 
-One STEP = one pass of every SURVEY §8(a) row over one batch of synthetic input (default
-workload C4, BASELINE.json configs[3]: d=10,000 random-walk streams, n=200,000, m=256, k=64,
-FP32, 20 injected discords):
+One STEP = one pass of every SURVEY §8(a) row over one batch of synthetic input.  Default
+workload C5 (BASELINE.json configs[4], the configuration BASELINE's metric "MP cell updates/s at
+1/2/4/8 B200" is quoted on: d=2,000 seasonal-plus-noise streams, n=2,000,000, m=256, k=32, FP32,
+50 injected discords); `--config c4` runs configs[3] (d=10,000 random walks, n=200,000, m=256,
+k=64, the dynamic add-500/delete-500 configuration):
   a2-a4  sketch_build over the d streams (count sketch, Alg. 1)
   a5     sketch_add_dim of 500 new streams + sketch_del_dim of 500 originals (§3.3)
   a6-a9  mp_create (window prep) + mp_join (the diagonal recurrence) + mp_finalize
@@ -15,7 +17,9 @@ Multi-GPU (torchrun, N>1): streams are sharded over ranks, partial sketches are 
 (NCCL), each rank joins its diagonal band (mp_band) and the profile keys are max-all-reduced
 (NCCL); every rank finalizes a slice of the windows (reduced to rank 0), rank 0 ranks the
 discords, and Alg. 3 runs on every rank's own streams of the group (all-gathered maxima).
-Strong scaling (fixed total work).
+Strong scaling (fixed total work).  `--gpus N` without a torchrun environment re-launches this
+script as N ranks (python -m torch.distributed.run --nproc-per-node N, 127.0.0.1); rank 0 prints
+the one JSON line.
 
 `value` = exact join cells per step (k (n_sub-r-1)(n_sub-r)/2) / device step time, inputs
 resident in HBM.  `e2e` = the same with the inputs in pinned HOST memory handed to the C-ABI
@@ -46,6 +50,8 @@ UNIT = "cell updates/s"
 FP32_PIPE_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # B200: 148 SMs x 128 FP32 lanes x FMA x max clock
 FLOPS_PER_CELL = 6                                    # 2 FFMA (4 flop) + 2 FMUL (2 flop), DESIGN.md §5
 FP64_PIPE_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+FFMA_MEASURED = 0.971    # FFMA warp-instructions / clk / SMSP measured (profiles/r1b_pipe_mix.txt)
+DFMA_MEASURED = 0.4865 / 0.5  # DFMA 0.4865 warp-instr / clk / SMSP of 0.5 (profiles/r1b_fp64_rate.txt)
 
 
 def log(*a):
@@ -55,16 +61,43 @@ def log(*a):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c4"))
+    ap.add_argument("--config", default=os.environ.get("BENCH_CONFIG", "c5"))
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--top", type=int, default=0, help="discords per step (default 2 x injected)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="pipelined e2e batches (default 5; 3 for C5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reseed", type=int, default=0)
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process group backend (gloo: the one-GPU multi-rank test, ranks share cuda:0)")
+    ap.add_argument("--shape", default="", help="test shapes: scale the config, e.g. d=200,n=20000,k=8")
+    ap.add_argument("--dump", default="", help="rank 0 writes the last step's keys / P / I / top-K here (.npz)")
     return ap.parse_args()
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: run this script as N ranks, one per GPU (the driver's own
+    launch line), and pass rank 0's JSON line through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("relaunch:", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def join_kernel_name(dtype: str) -> str:
@@ -189,7 +222,8 @@ def run_reference(args, cfg, top):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": workload_desc(cfg, top)},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu": cpu_model(), "kind": "oracle",
+                            "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -200,9 +234,15 @@ def run_reference(args, cfg, top):
 # ----------------------------------------------------------------------------------------------
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(args)
     import synthgen
     cfg = synthgen.CONFIGS[args.config]
+    if args.shape:
+        cfg = synthgen.scaled(cfg, **{kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.shape.split(",")})
     top = args.top or max(3, 2 * cfg.n_discords)
+    if args.e2e_steps <= 0:
+        args.e2e_steps = 3 if cfg.n * cfg.d >= 4_000_000_000 else 5
     if args.impl == "reference":
         return run_reference(args, cfg, top)
 
@@ -216,10 +256,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.backend == "gloo":   # test mode: every rank on one GPU, collectives staged via host
+        local = local % torch.cuda.device_count()
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPUs "
+                         "(one process per GPU; --backend gloo shares one GPU for tests)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     skmp.lib()
     tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
     dcode = skmp.F32 if cfg.dtype == "f32" else skmp.F64
@@ -262,6 +310,7 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     S_dense = synthgen.dense_S(cfg)[:, [int(j) for j in my_ids]] if cfg.proj == "dense" else None
+    dumpbox: dict = {}
 
     def build(T):
         if S_dense is not None:  # C1's Gaussian projection (reading 1)
@@ -288,6 +337,9 @@ def main():
         if world > 1:
             sdist.allreduce_sketch(sk)
         if e: e[2].record()
+        if args.dump:
+            dumpbox["R"] = sk.R.cpu().numpy()
+            dumpbox["R64"] = sk.R64.cpu().numpy()
         w = skmp.mp_create(sk.R, m, reseed_rows=args.reseed)
         if e: e[3].record()
         for lo, hi in ranges:
@@ -299,6 +351,8 @@ def main():
         if world > 1:
             keys, words = skmp.mp_keys(w)
             sdist.reduce_keys(keys, words)
+        if args.dump:
+            dumpbox["keys"] = skmp.mp_keys(w)[0].cpu().numpy()
         res = None
         if world > 1:  # every rank resolves a slice of the windows, P / I reduced to rank 0
             fin = sdist.finalize_dist(w)
@@ -307,12 +361,16 @@ def main():
         if rank == 0:
             P, I, inert = fin
             res = skmp.discord_topk(P, I, inert, m=m, top=top)
+            if args.dump:
+                dumpbox.update(P=P.cpu().numpy(), I=I.cpu().numpy(), inert=inert,
+                               top=np.array([(d.t, d.g, d.nn) for d in res]),
+                               top_score=np.array([d.score for d in res]))
         w.free()
         if e: e[5].record()
         # Alg. 3: the dimension j* of the top discord inside its group J_g*
         tg = torch.tensor([res[0].t, res[0].g] if rank == 0 else [0, 0], dtype=torch.int64, device=dev)
         if world > 1:
-            dist.broadcast(tg, 0)
+            sdist.broadcast(tg, 0)
         t_star, g_star = (int(x) for x in tg.tolist())
         sources = [(T, my_ids), (Ta, my_add)]
         if world > 1:
@@ -320,6 +378,9 @@ def main():
         else:
             dim = skmp.detect_dimension(sk, sources, t_star, g_star, m)
         sk.free()
+        if args.dump:
+            dumpbox["dim"] = np.array([] if dim is None else [dim[0], dim[2]], dtype=np.uint64)
+            dumpbox["dim_score"] = np.array([] if dim is None else [dim[1]])
         if e:
             e[6].record()
             timers.append(e)
@@ -360,7 +421,7 @@ def main():
     }
     t = torch.tensor([elapsed_ms, phase["mp_join_ms"]], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sdist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_ms, join_ms_max = float(t[0]), float(t[1])
     ms_per_step = elapsed_ms / args.steps
     value = cells_total / (ms_per_step / 1e3)
@@ -369,9 +430,11 @@ def main():
     e2e = None
     if not args.no_e2e and host_T is None:
         try:  # pinned host copies of the device-generated inputs (needs ~d*n*4 bytes of host RAM)
-            host_T = Td.cpu().pin_memory()
-            host_add = Tadd.cpu().pin_memory() if Tadd is not None else None
-            host_del = Tdel.cpu().pin_memory() if Tdel is not None else None
+            def pinned(x):
+                return torch.empty(x.shape, dtype=x.dtype, pin_memory=True).copy_(x)
+            host_T = pinned(Td)
+            host_add = pinned(Tadd) if Tadd is not None else None
+            host_del = pinned(Tdel) if Tdel is not None else None
         except RuntimeError as ex:
             log(f"[rank {rank}] e2e skipped: {ex}")
     dim_rows = None
@@ -385,7 +448,7 @@ def main():
             skmp.sketch_del_dim(gsk, Tdel, my_del)
         gt = torch.tensor([res[0][0].g if rank == 0 else 0], dtype=torch.int64, device=dev)
         if world > 1:
-            dist.broadcast(gt, 0)
+            sdist.broadcast(gt, 0)
         dim_rows = len(skmp.group_rows(gsk, int(gt.item())))
         gsk.free()
         pf = Prefetcher(dev)
@@ -430,7 +493,7 @@ def main():
                 log(f"  B stage {b}: {s0.elapsed_time(x):7.1f} -> {s0.elapsed_time(y):7.1f}")
         et = torch.tensor([s0.elapsed_time(s1)], device=dev, dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            sdist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et[0]) / args.e2e_steps
         esz = host_T.element_size()
         h2d = (host_T.numel() + (0 if host_add is None else host_add.numel())
@@ -438,7 +501,7 @@ def main():
         h2d += dim_rows * cfg.n * esz  # Alg. 3 stages its group's host rows
         if world > 1:
             hb = torch.tensor([h2d], device=dev, dtype=torch.float64)
-            dist.all_reduce(hb)
+            sdist.all_reduce(hb)
             h2d = int(hb.item())
         d2h = top * (8 + 4 + 8 + 8) + 4 + 16  # top-K tuples + count + Alg. 3 result
         e2e = {"value": cells_total / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -450,6 +513,8 @@ def main():
     if rank != 0:
         dist.destroy_process_group()
         return 0
+    if args.dump:
+        np.savez(args.dump, **dumpbox)
 
     # ---------------- roofline of the dominant kernel (the join) ----------------
     pk = peaks()
@@ -483,7 +548,11 @@ def main():
                              f"mp_join event time; peak = 148 SM x {128 if cfg.dtype == 'f32' else 64} lanes x 2 x "
                              f"1.965 GHz (derived, DESIGN.md §5)",
                      "pipe_frac": (cells_band / (phase['mp_join_ms'] / 1e3)) * 4 /
-                                  (148 * (128 if cfg.dtype == 'f32' else 64) * 1.965e9)},
+                                  (148 * (128 if cfg.dtype == 'f32' else 64) * 1.965e9),
+                     "peak_measured": peak * (FFMA_MEASURED if cfg.dtype == "f32" else DFMA_MEASURED),
+                     "peak_measured_note": "dependent-chain microbenchmark on one B200 (FFMA 0.971 warp-instr/clk/SMSP, "
+                                           "profiles/r1b_pipe_mix.txt; DFMA profiles/r1b_fp64_rate.txt): the issue "
+                                           "rate a plain FMA stream actually reaches; frac is against the derived peak"},
         "sketch": {"bound": "hbm", "achieved": sk_gbs, "peak": hbm_peak, "unit": "GB/s",
                    "frac": sk_gbs / hbm_peak, "bytes_per_build": sk_bytes,
                    "note": "algorithmic bytes 2 d n b + k n (8 + b) over sketch_build event time (includes its "
@@ -503,7 +572,7 @@ def main():
         threads = len(os.sched_getaffinity(0))
         v, nrows, dt = oracle_sample(cfg, 12.0, threads)
         out["cpu_baseline"] = {
-            "value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "value": v, "unit": UNIT, "cores": threads, "cpu": cpu_model(), "kind": "oracle",
             "sample": f"oracle/mp_brute.c brute force on {nrows} random whole rows of one n={cfg.n}, m={cfg.m} "
                       f"series ({dt:.1f} s); cells = rows x admissible pairs / 2"}
     print(json.dumps(out), flush=True)

@@ -1,6 +1,7 @@
 /* Plain-C consumer of the C-ABI (no Python, no torch): sketch d random walks from HOST memory
- * (Alg. 1), self-join every sketch series (Def. 6), rank the discords (Alg. 2), and check the top
- * discord's profile value against a brute force over its group's sketch series.
+ * (Alg. 1), self-join every sketch series (Def. 6), rank the discords (Alg. 2), find the top
+ * discord's dimension inside its group (Alg. 3, discord_dims_group), and check the top discord's
+ * profile value and the dimension against brute forces over the sketch series / raw streams.
  *
  *   gcc -std=c99 -O2 examples/abi_demo.c -Iinclude -I/usr/local/cuda/include \
  *       -Lpaper_2311_03393_b200 -lsketchmp -L/usr/local/cuda/lib64 -lcudart -lm \
@@ -102,7 +103,35 @@ int main(void) {
   printf("brute force %.6f, library %.6f, rel err %.2e; planted burst at t=1700 in stream 5\n", best, score[0], rel);
   int planted = 0; /* the burst is among the top discords (random walks have large scores too) */
   for (int q = 0; q < found; ++q) planted |= llabs(t_out[q] - 1700) <= m;
-  const int ok = found == top && rel <= 1e-9 && planted;
+
+  /* Alg. 3: the dimension of the top discord inside J_{g*} (the raw streams, one host source) */
+  skmp_source src = {T, n, d, ids};
+  skmp_dim_result dim;
+  CHECK(discord_dims_group(sk, g_out[0], &src, 1, t_out[0], m, -1, &dim, NULL));
+  int32_t* gp = (int32_t*)malloc(sizeof(int32_t) * d);
+  CHECK(sketch_plan(sk, NULL, gp, NULL, NULL, NULL));
+  double bs = -INFINITY;
+  uint64_t bid = 0;
+  int64_t members = 0;
+  for (int64_t j = 0; j < d; ++j) { /* plan order = input order; first strict maximiser */
+    if (gp[j] != g_out[0]) continue;
+    ++members;
+    double s1 = INFINITY;
+    for (int64_t u = 0; u < n_sub; ++u) {
+      const int64_t du = u > t_out[0] ? u - t_out[0] : t_out[0] - u;
+      if (du <= excl) continue;
+      const double v = zdist(T + j * n, t_out[0], u, m);
+      if (v < s1) s1 = v;
+    }
+    if (s1 > bs) { bs = s1; bid = ids[j]; }
+  }
+  const double rel3 = fabs(bs - dim.score) / bs;
+  printf("Alg. 3: j* = id %llu (score %.6f, nn %lld, %lld members); brute force id %llu score %.6f\n",
+         (unsigned long long)dim.id, dim.score, (long long)dim.nn, (long long)dim.n_scored,
+         (unsigned long long)bid, bs);
+  const int ok = found == top && rel <= 1e-9 && planted && dim.n_scored == members && dim.id == bid &&
+                 rel3 <= 1e-9;
+  free(gp);
   cudaFree(P);
   cudaFree(I);
   sketch_free(sk);

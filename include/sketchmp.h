@@ -44,7 +44,7 @@ typedef enum {
   SKMP_E_LENGTH_MISMATCH = 8,  /* added/deleted streams must span the full n     */
   SKMP_E_ALL_GROUPS_INERT = 9, /* every sketch group empty or flat         reading 10         */
   SKMP_E_CUDA = 10,            /* CUDA runtime error (incl. no device)                         */
-  SKMP_E_NCCL = 11,            /* reserved: collective errors (multi-GPU reduce lives above)  */
+  SKMP_E_NCCL = 11,            /* NCCL failure or libnccl missing (native multi-GPU calls)    */
   SKMP_E_OOM = 12              /* device allocation failed                                     */
 } skmp_status;
 
@@ -60,6 +60,12 @@ int64_t skmp_last_error_index(void);             /* offending stream/group/row, 
 int32_t skmp_abi_version(void);                  /* SKMP_ABI_VERSION                           */
 int64_t skmp_launch_count(void);                 /* kernels this library launched so far (all  */
                                                  /* threads); bench.py reports the delta       */
+/* Device memory: the library allocates only from two stream-ordered pools of its own per device
+ * (work: handles, workspaces, per-call temporaries; staging: host-input copies), never from the
+ * process's default pool, and keeps freed blocks cached between calls.  skmp_trim() returns every
+ * cached, unused block of those pools to the device (memory still owned by live handles stays).
+ * Callable without a GPU (then a no-op).  Errors: CUDA. */
+skmp_status skmp_trim(void);
 
 /* ---------------------------------------------------------------------------------------------
  * Hash plan (host-only; callable without a GPU).  The count-sketch pair (h, s) of P:L200-204
@@ -141,7 +147,13 @@ skmp_status sketch_plan(const skmp_sketch* h, uint64_t* ids, int32_t* g, int8_t*
 /* Re-round R = dtype(R64) after R64 was modified outside the library (e.g. a cross-GPU
  * sum-allreduce of per-rank partial sketches).  Asynchronous. */
 skmp_status sketch_refresh(skmp_sketch* h, void* stream);
+/* Release the handle.  The device memory is freed stream-ordered on the stream of the last
+ * library call that used the handle; a caller that read R / R64 on ANOTHER stream (e.g. a sketch
+ * built on a prefetch stream and joined on the main stream) must call sketch_free_async with
+ * that stream, which frees after both the handle's own work and everything already enqueued on
+ * `stream`. */
 void sketch_free(skmp_sketch* h);
+void sketch_free_async(skmp_sketch* h, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * Matrix-profile self-join over each sketch series (Def. 6; self-join variant
@@ -309,8 +321,8 @@ void stream_free(skmp_stream* h);
  *                       assembles P, I on EVERY rank (bit-identical to mp_selfjoin).  Arguments
  *                       as mp_selfjoin; every rank must pass the same R contents and sizes.
  * NCCL is loaded with dlopen("libnccl.so.2") on first use (a process that already holds one
- * reuses it).  Errors: INVALID_ARG, CUDA (incl. NCCL failures and a missing libnccl), OOM and
- * those of the composed calls.  A rank that fails returns without entering the remaining
+ * reuses it).  Errors: INVALID_ARG, NCCL (a collective or communicator failure, or libnccl.so.2
+ * missing or incomplete), CUDA, OOM and those of the composed calls.  A rank that fails returns without entering the remaining
  * collectives: callers pass identical arguments so that all ranks fail alike. */
 typedef struct skmp_comm skmp_comm;
 skmp_status skmp_comm_unique_id(uint8_t id[128]);
@@ -344,7 +356,8 @@ skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, 
  * for each listed stream j of the discord's group J_{g*} (dist = z-normalised Euclidean, Def. 3
  * P:L129-133, evaluated by explicit differences in FP64; flat windows per reading 5 relative
  * to max|T_j|; smallest t on ties), and j* = the FIRST strict maximiser in the listed order
- * (Alg. 3 lines 3-7, reading 20).  The refinement join of P:L303-304 is mp_selfjoin on row j*.
+ * (Alg. 3 lines 3-7, reading 20).  The refinement join of P:L303-304 is mp_selfjoin on row j*
+ * followed by discord_topk with top = 1.
  *   T       [dev|host] (max(rows)+1) x ld streams (dtype), n samples each (a host matrix is
  *           staged row by row: only the listed rows cross PCIe).
  *   rows    [host] nrows stream rows of T (the members of J_{g*}, in group order).
@@ -357,6 +370,45 @@ skmp_status discord_topk(const void* P, const int64_t* I, const uint8_t* inert, 
 skmp_status discord_dims(const void* T, int64_t ld, int64_t n, int32_t dtype, const int64_t* rows,
                          int64_t nrows, int64_t t_star, int32_t m, int32_t excl, double* scores,
                          int64_t* nn, int64_t* j_star, void* stream);
+
+/* Alg. 3 over the discord's group J_{g*} of a sketch, with the raw streams spread over several
+ * matrices (Alg. 3 lines 1-2 take "the dimensions in group g*" and line 3 scans them
+ * in order).  Members of J_g are taken in the sketch plan's order (sketch_plan: input order, added
+ * streams appended, deleted ones removed; DENSE: every stream, reading 1); each member is scored
+ * in the first source whose ids list it, as discord_dims scores a row (same definition, tie and
+ * flat rules); members no source holds are skipped, so a rank of a stream-sharded sketch scores
+ * its own streams only.  The winner is the FIRST strict maximiser in plan order (reading 20).
+ *   h       the sketch whose plan defines J_g (not modified; its R is not read).
+ *   g       the group (count sketch: 0 <= g < k; ignored for DENSE).
+ *   src     [host] nsrc sources {T [dev|host] rows x ld (the sketch's dtype, the sketch's n samples
+ *           per stream), ld >= n, rows, ids [host] rows stream ids}; nsrc may be 0.
+ *   out     [host, out] {score, id, nn, n_scored}: n_scored = members scored; when it is 0 the
+ *           other fields are left untouched.
+ * Synchronous.  Errors: INVALID_ARG (NULL, bad g, bad source, bad t_star, m < 2),
+ * SERIES_TOO_SHORT, NO_ADMISSIBLE, CUDA, OOM. */
+typedef struct {
+  const void* T;        /* [dev|host] rows x ld streams                                        */
+  int64_t ld;           /* leading dimension in elements, >= the sketch's n                    */
+  int64_t rows;         /* number of streams in T                                             */
+  const uint64_t* ids;  /* [host] rows: stream id of each row                                  */
+} skmp_source;
+
+typedef struct {
+  double score;         /* s^(j*): 1NN distance of T_{j*, t*, m} in its own stream            */
+  uint64_t id;          /* j*: the winning stream's id                                         */
+  int64_t nn;           /* its nearest neighbour's window start                               */
+  int64_t n_scored;     /* members of J_g scored (0: no winner, other fields untouched)        */
+} skmp_dim_result;
+
+skmp_status discord_dims_group(const skmp_sketch* h, int32_t g, const skmp_source* src, int32_t nsrc,
+                               int64_t t_star, int32_t m, int32_t excl, skmp_dim_result* out, void* stream);
+
+/* Host-only: combine per-part Alg. 3 winners (parts[q] from discord_dims_group over disjoint
+ * pieces of J_g that come in J_g order, e.g. ranks holding contiguous id shards, in rank order):
+ * out = the first part with the strictly largest score among parts with n_scored > 0, and
+ * out->n_scored = the total.  The multi-GPU path all-gathers the ranks' results and calls this.
+ * Errors: INVALID_ARG (NULL, nparts < 1, negative n_scored). */
+skmp_status discord_dims_merge(const skmp_dim_result* parts, int32_t nparts, skmp_dim_result* out);
 
 #ifdef __cplusplus
 }

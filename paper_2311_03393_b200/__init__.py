@@ -50,6 +50,17 @@ class SketchCfg(ctypes.Structure):
                 ("groups", ctypes.c_void_p), ("signs", ctypes.c_void_p), ("S", ctypes.c_void_p)]
 
 
+class Source(ctypes.Structure):
+    """skmp_source: one matrix of raw streams for discord_dims_group."""
+    _fields_ = [("T", ctypes.c_void_p), ("ld", ctypes.c_int64), ("rows", ctypes.c_int64), ("ids", ctypes.c_void_p)]
+
+
+class DimResult(ctypes.Structure):
+    """skmp_dim_result: Alg. 3's winner (score, id, nn) and how many members were scored."""
+    _fields_ = [("score", ctypes.c_double), ("id", ctypes.c_uint64), ("nn", ctypes.c_int64),
+                ("n_scored", ctypes.c_int64)]
+
+
 class MpCfg(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int32), ("excl", ctypes.c_int32), ("reseed_rows", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
@@ -106,6 +117,10 @@ _SIGS = {
     "sketch_allreduce": (ctypes.c_int, [_P, _P, _P]),
     "mp_selfjoin_dist": (ctypes.c_int, [_P, _P, _I32, _I64, _I64, _I32, ctypes.POINTER(MpCfg), _P, _P, _P, _P]),
     "discord_dims": (ctypes.c_int, [_P, _I64, _I64, _I32, _P, _I64, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "discord_dims_group": (ctypes.c_int, [_P, _I32, _P, _I32, _I64, _I32, _I32, ctypes.POINTER(DimResult), _P]),
+    "discord_dims_merge": (ctypes.c_int, [_P, _I32, ctypes.POINTER(DimResult)]),
+    "skmp_trim": (ctypes.c_int, []),
+    "sketch_free_async": (None, [_P, _P]),
 }
 
 
@@ -206,9 +221,11 @@ class Sketch:
     def __init__(self, handle):
         self.handle = handle
 
-    def free(self):
+    def free(self, stream=None):
+        """Free stream-ordered after the handle's own work and everything already enqueued on
+        `stream` (default: torch's current stream, where the caller read R)."""
         if self.handle:
-            lib().sketch_free(self.handle)
+            lib().sketch_free_async(self.handle, _stream(stream))
             self.handle = None
 
     def __del__(self):
@@ -319,6 +336,11 @@ def sketch_refresh(sk: Sketch, stream=None):
 
 def skmp_launch_count() -> int:
     return int(lib().skmp_launch_count())
+
+
+def skmp_trim():
+    """Return the library pools' cached, unused device memory (C-ABI skmp_trim)."""
+    _check(lib().skmp_trim())
 
 
 def sketch_free(sk: Sketch):
@@ -557,11 +579,18 @@ class Stream:
         cfg = _mpcfg(m, -1, reseed_rows)
         h = ctypes.c_void_p()
         _check(lib().stream_create(train.handle, ctypes.byref(cfg), capacity, _stream(stream), ctypes.byref(h)))
-        _, k, _, _, dt = sketch_view(train)
-        self.handle, self.m, self.k, self.cap, self.dtype = h, m, k, capacity, dt
+        _, k, _, d, dt = sketch_view(train)
+        self.handle, self.m, self.k, self.cap, self.dtype, self.d = h, m, k, capacity, dt, d
 
     def push(self, T, stream=None):
         """T: d x n_new (torch CUDA tensor or numpy array, train dtype), rows in the plan order."""
+        try:
+            dc = _dtype_code(T)
+        except ValueError:
+            dc = -1
+        if T.ndim != 2 or T.shape[0] != self.d or dc != self.dtype:
+            raise SkmpError(1, f"Stream.push: T must be {self.d} x n_new of the train sketch's dtype "
+                               f"({'float32' if self.dtype == F32 else 'float64'}), got {tuple(T.shape)} {T.dtype}", -1)
         n_new = T.shape[1]
         ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
         _check(lib().stream_push(self.handle, _ptr(T), n_new, ld, _stream(stream)))
@@ -624,29 +653,41 @@ def discord_dims(T, rows, t_star: int, m: int, excl: int = -1, n: int | None = N
     return sc, nn, int(js.value)
 
 
-def detect_dimension(sk: Sketch, sources, t: int, g: int, m: int, excl: int = -1, stream=None):
-    """Alg. 3 over J_g for the discord at time t, with the group's streams spread over several
-    device matrices: `sources` = [(T, ids), ...] (rows of T hold the streams with those ids).
-    Returns (id*, score, nn) with Alg. 3's tie rule (first strict maximiser in plan order), or
-    None when no stream of J_g is in `sources`."""
-    pl = sketch_plan(sk)
-    members = pl["ids"] if np.all(pl["groups"] < 0) else pl["ids"][pl["groups"] == g]
-    order = {int(j): q for q, j in enumerate(members)}
-    best = None
+def discord_dims_group(sk: Sketch, g: int, sources, t_star: int, m: int, excl: int = -1, stream=None) -> DimResult:
+    """Alg. 3 over J_g of the sketch plan with the raw streams spread over several matrices
+    (C-ABI discord_dims_group): `sources` = [(T, ids), ...] (rows of T hold the streams with
+    those ids; T a CUDA tensor or a host array, None / empty skipped).  Returns the DimResult
+    (n_scored == 0: no member of J_g in `sources`)."""
+    keep, arr = [], []
     for T, ids in sources:
-        if T is None or len(ids) == 0:
+        if T is None or ids is None or len(ids) == 0:
             continue
-        ids = np.asarray(ids, dtype=np.uint64)
-        rows = np.array([q for q, j in enumerate(ids) if int(j) in order], dtype=np.int64)
-        if len(rows) == 0:
-            continue
-        sc, nn, _ = discord_dims(T, rows, t, m, excl, stream=stream)
-        for q in range(len(rows)):
-            j = int(ids[rows[q]])
-            cand = (float(sc[q]), -order[j], j, int(nn[q]))
-            if best is None or cand[:2] > best[:2]:
-                best = cand
-    return None if best is None else (best[2], best[0], best[3])
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        assert T.shape[0] == len(ids), "one id per row of T"
+        ld = T.stride(0) if hasattr(T, "stride") and callable(T.stride) else T.strides[0] // T.itemsize
+        keep.append(ids)
+        arr.append(Source(_ptr(T).value, ld, len(ids), ids.ctypes.data))
+    src = (Source * max(1, len(arr)))(*arr)
+    out = DimResult()
+    _check(lib().discord_dims_group(sk.handle, g, ctypes.cast(src, _P), len(arr), t_star, m, excl, ctypes.byref(out),
+                                    _stream(stream)))
+    return out
+
+
+def discord_dims_merge(parts) -> DimResult:
+    """Host-only: the first strict maximum over per-part winners in J_g order (C-ABI)."""
+    arr = (DimResult * len(parts))(*parts)
+    out = DimResult()
+    _check(lib().discord_dims_merge(ctypes.cast(arr, _P), len(parts), ctypes.byref(out)))
+    return out
+
+
+def detect_dimension(sk: Sketch, sources, t: int, g: int, m: int, excl: int = -1, stream=None):
+    """Alg. 3 over J_g for the discord at time t (discord_dims_group).  Returns (id*, score, nn)
+    with Alg. 3's tie rule (first strict maximiser in plan order), or None when no stream of J_g
+    is in `sources`."""
+    r = discord_dims_group(sk, g, sources, t, m, excl, stream)
+    return None if r.n_scored == 0 else (int(r.id), float(r.score), int(r.nn))
 
 
 @dataclass
@@ -679,20 +720,19 @@ def detect(T, ids, k: int, m: int, *, seed: int = 0, proj: int = PROJ_COUNT_SKET
     P, I, inert = mp_selfjoin(sk.R, m, stream=stream)
     top = discord_topk(P, I, inert, m=m, top=1, stream=stream)[0]
     ev[2].record()
-    rows = group_rows(sk, top.g)
-    sc, nn, js = discord_dims(T, rows, top.t, m, stream=stream)
+    ids_a = np.ascontiguousarray(ids, dtype=np.uint64)
+    dim = discord_dims_group(sk, top.g, [(T, ids_a)], top.t, m, stream=stream)
     ev[3].record()
-    j = int(rows[js])
     rt = rs = None
-    if refine:
-        Pj, _, _ = mp_selfjoin(T[j:j + 1], m, stream=stream)
-        rt = int(torch.argmax(Pj[0]))
-        rs = float(Pj[0, rt])
+    if refine:  # the full profile of stream j* and its top-1 discord (discord_topk)
+        j = int(np.nonzero(ids_a == dim.id)[0][0])
+        Pj, Ij, inj = mp_selfjoin(T[j:j + 1], m, stream=stream)
+        d1 = discord_topk(Pj, Ij, inj, m, 1, stream=stream)[0]
+        rt, rs = d1.t, d1.score
     ev[4].record()
     torch.cuda.synchronize()
-    ids_a = np.asarray(ids)
     sk.free()
     ms = {"sketch": ev[0].elapsed_time(ev[1]), "time_detection": ev[1].elapsed_time(ev[2]),
           "dimension_detection": ev[2].elapsed_time(ev[3]), "refine": ev[3].elapsed_time(ev[4])}
-    return DiscordReport(top.t, top.g, top.score, int(ids_a[j]), float(sc[js]), int(nn[js]), rt, rs, ms)
+    return DiscordReport(top.t, top.g, top.score, int(dim.id), float(dim.score), int(dim.nn), rt, rs, ms)
 

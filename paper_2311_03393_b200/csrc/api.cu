@@ -41,6 +41,17 @@ skmp_status cuda_error(cudaError_t e, const char* where) {
 }
 }  // namespace skmp
 
+namespace {
+cudaMemPool_t work_pool_impl();
+}
+
+namespace skmp {
+cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = work_pool_impl();
+  return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
+}  // namespace skmp
+
 using namespace skmp;
 
 namespace {
@@ -57,18 +68,6 @@ skmp_status require_device() {
   if (e != cudaSuccess || n == 0) {
     cudaGetLastError();
     return set_error(SKMP_E_CUDA, "no CUDA device available (the path has no CPU fallback)");
-  }
-  // keep stream-ordered temporaries cached in the device pool between calls (no OS round trip)
-  static thread_local int configured = -1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess && configured != dev) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-    configured = dev;
   }
   return SKMP_OK;
 }
@@ -96,7 +95,7 @@ struct Temps {
   cudaError_t alloc(T** p, size_t count, cudaMemPool_t pool = nullptr) {
     void* q = nullptr;
     cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, count * sizeof(T) + 16, pool, st)
-                         : cudaMallocAsync(&q, count * sizeof(T) + 16, st);
+                         : dmalloc(&q, count * sizeof(T) + 16, st);
     if (e == cudaSuccess) {
       ptrs.push_back(q);
       *p = static_cast<T*>(q);
@@ -105,18 +104,32 @@ struct Temps {
   }
 };
 
-// Host-input staging buffers come from a pool of their own (one per device, never trimmed):
-// multi-GB staging blocks interleaved with the small workspaces of the default pool fragmented
-// it, so a later staging allocation could miss a contiguous block and grow the pool (mapping
-// gigabytes of fresh memory) in the middle of a pipelined batch.
-cudaMemPool_t staging_pool() {
-  static std::mutex mu;
-  static std::vector<cudaMemPool_t> pools;
+// The library's device memory comes from two pools of its own per device (never the process's
+// default pool, whose attributes belong to the caller): the WORK pool (handles, workspaces and
+// per-call temporaries) and the STAGING pool (host-input staging buffers).  Both keep freed
+// blocks cached (release threshold = max) so repeated calls do not round-trip to the OS;
+// skmp_trim() returns the cached memory.  Staging has its own pool because multi-GB staging
+// blocks interleaved with the small workspaces fragmented a shared pool, so a later staging
+// allocation could miss a contiguous block and grow the pool (mapping gigabytes of fresh memory)
+// in the middle of a pipelined batch.
+struct Pools {
+  std::mutex mu;
+  std::vector<cudaMemPool_t> work, staging;
+};
+Pools& pools() {
+  static Pools p;
+  return p;
+}
+
+cudaMemPool_t make_pool(std::vector<cudaMemPool_t>& v) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if ((int)pools.size() <= dev) pools.resize((size_t)dev + 1, nullptr);
-  if (!pools[(size_t)dev]) {
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(pools().mu);
+  if ((int)v.size() <= dev) v.resize((size_t)dev + 1, nullptr);
+  if (!v[(size_t)dev]) {
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.handleTypes = cudaMemHandleTypeNone;
@@ -125,14 +138,17 @@ cudaMemPool_t staging_pool() {
     cudaMemPool_t p = nullptr;
     if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
       cudaGetLastError();
-      return nullptr;  // fall back to the default pool
+      return nullptr;  // then the runtime's default pool (cudaMallocAsync)
     }
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
-    pools[(size_t)dev] = p;
+    v[(size_t)dev] = p;
   }
-  return pools[(size_t)dev];
+  return v[(size_t)dev];
 }
+
+cudaMemPool_t staging_pool() { return make_pool(pools().staging); }
+cudaMemPool_t work_pool_impl() { return make_pool(pools().work); }
 
 // Stage a (possibly host) rows x ld matrix into device memory; returns the device pointer.
 skmp_status stage_input(const void* T, int64_t rows, int64_t n, int64_t ld, int dtype, Temps& tmp,
@@ -386,9 +402,9 @@ skmp_status sketch_build(const void* T, int64_t d, int64_t n, int64_t ld, const 
   h->n = n;
   h->seed = cfg->seed;
   h->st = st;
-  cudaError_t e = cudaMallocAsync((void**)&h->R64, sizeof(double) * (size_t)h->k * n, st);
+  cudaError_t e = dmalloc((void**)&h->R64, sizeof(double) * (size_t)h->k * n, st);
   if (e == cudaSuccess && h->dtype == SKMP_F32)
-    e = cudaMallocAsync(&h->R, sizeof(float) * (size_t)h->k * n, st);
+    e = dmalloc(&h->R, sizeof(float) * (size_t)h->k * n, st);
   if (e != cudaSuccess) {
     sketch_free(h);
     return cuda_error(e, "sketch_build: allocate R");
@@ -606,6 +622,33 @@ void sketch_free(skmp_sketch* h) {
   delete h;
 }
 
+void sketch_free_async(skmp_sketch* h, void* stream) {
+  if (!h) return;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (st != h->st) {  // free after the handle's own work AND everything already queued on `stream`
+    cudaEvent_t ev;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+      if (cudaEventRecord(ev, h->st) == cudaSuccess) cudaStreamWaitEvent(st, ev, 0);
+      cudaEventDestroy(ev);
+    }
+    cudaGetLastError();
+    h->st = st;
+  }
+  sketch_free(h);
+}
+
+skmp_status skmp_trim(void) {
+  Pools& p = pools();
+  std::lock_guard<std::mutex> lock(p.mu);
+  for (auto* v : {&p.work, &p.staging})
+    for (cudaMemPool_t q : *v)
+      if (q) {
+        cudaError_t e = cudaMemPoolTrimTo(q, 0);
+        if (e != cudaSuccess) return cuda_error(e, "skmp_trim: cudaMemPoolTrimTo");
+      }
+  return ok();
+}
+
 }  // extern "C"
 
 // ============================================================================================
@@ -691,7 +734,7 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   const size_t oQ = take(qsz * kq), oMu = take(8 * kq), oSig = take(8 * kq), oFlat = take(kq),
                oAmax = take(8 * (size_t)k), oNf = take(4 * (size_t)k),
                oKeys = take(8 * (size_t)words * (size_t)k * (size_t)w.n_sub);
-  cudaError_t e = cudaMallocAsync(&h->base, off, st);
+  cudaError_t e = dmalloc(&h->base, off, st);
   if (e != cudaSuccess) {
     delete h;
     return cuda_error(e, "mp_create: allocate workspace");
@@ -723,7 +766,7 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
     any_flat |= h->nflat[(size_t)g] > 0;
   }
   if (any_flat) {
-    e = cudaMallocAsync((void**)&w.flat_list, sizeof(int32_t) * (size_t)k * (size_t)w.n_sub, st);
+    e = dmalloc((void**)&w.flat_list, sizeof(int32_t) * (size_t)k * (size_t)w.n_sub, st);
     if (e == cudaSuccess) e = launch_flat_lists(w, h->nflat.data(), st);
     if (e != cudaSuccess) {
       mp_free(h);
@@ -1065,14 +1108,14 @@ skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int6
   h->cfg = *cfg;
   h->nflat.assign((size_t)train->k, 0);
   const size_t es = elem_size(train->dtype), kc = (size_t)train->k * (size_t)capacity;
-  cudaError_t e = cudaMallocAsync((void**)&q.R64, sizeof(double) * kc, st);
+  cudaError_t e = dmalloc((void**)&q.R64, sizeof(double) * kc, st);
   if (e == cudaSuccess) {
-    if (q.dtype == SKMP_F32) e = cudaMallocAsync(&q.R, sizeof(float) * kc, st);
+    if (q.dtype == SKMP_F32) e = dmalloc(&q.R, sizeof(float) * kc, st);
     else q.R = q.R64;
   }
-  if (e == cudaSuccess) e = cudaMallocAsync(&h->P, es * kc, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->I, sizeof(int64_t) * kc, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&h->Rtrain, es * (size_t)train->k * (size_t)train->n, st);
+  if (e == cudaSuccess) e = dmalloc(&h->P, es * kc, st);
+  if (e == cudaSuccess) e = dmalloc((void**)&h->I, sizeof(int64_t) * kc, st);
+  if (e == cudaSuccess) e = dmalloc(&h->Rtrain, es * (size_t)train->k * (size_t)train->n, st);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(h->Rtrain, train->R, es * (size_t)train->k * (size_t)train->n, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) {
@@ -1087,9 +1130,9 @@ skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int6
   // carried-path state: FP64 train records only for FP64 streams (FP32 streams use the train
   // workspace's own FP32 records); rings of one value per diagonal in the stream's dtype
   const size_t nring = (size_t)train->k * (size_t)h->train->w.n_sub;
-  e = cudaMallocAsync((void**)&h->ring[0], es * nring, st);
-  if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->ring[1], es * nring, st);
-  if (e == cudaSuccess && train->dtype == SKMP_F64) e = cudaMallocAsync(&h->q64, stream_q64_bytes(h->train->w), st);
+  e = dmalloc((void**)&h->ring[0], es * nring, st);
+  if (e == cudaSuccess) e = dmalloc((void**)&h->ring[1], es * nring, st);
+  if (e == cudaSuccess && train->dtype == SKMP_F64) e = dmalloc(&h->q64, stream_q64_bytes(h->train->w), st);
   if (e == cudaSuccess && train->dtype == SKMP_F64) e = launch_train_q64(h->train->w, h->q64, st);
   if (e != cudaSuccess) {
     stream_free(h);
@@ -1248,6 +1291,61 @@ void stream_free(skmp_stream* h) {
   delete h;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Alg. 3 lines 3-7: the first strict maximiser in order (reading 20: the scan starts from -inf)
+int64_t first_strict_max(const std::vector<double>& v) {
+  int64_t best = -1;
+  for (size_t q = 0; q < v.size(); ++q)
+    if (best < 0 || v[q] > v[(size_t)best]) best = (int64_t)q;
+  return best;
+}
+
+skmp_status dims_validate(const char* who, int64_t n, int64_t t_star, int m, int excl, int* ex) {
+  if (n < m) return set_error(SKMP_E_SERIES_TOO_SHORT, std::string(who) + ": n < m");
+  const int64_t n_sub = n - m + 1;
+  if (t_star < 0 || t_star >= n_sub)
+    return set_error(SKMP_E_INVALID_ARG, std::string(who) + ": t_star outside [0, n-m+1)", t_star);
+  *ex = excl < 0 ? (m + 1) / 2 : excl;
+  if (t_star - *ex - 1 < 0 && t_star + *ex + 1 >= n_sub)
+    return set_error(SKMP_E_NO_ADMISSIBLE, std::string(who) + ": no window farther than excl from t_star");
+  return SKMP_OK;
+}
+
+// K9 over the listed rows of one source matrix into d_score / d_nn (device, rows.size() each);
+// a host matrix is staged row by row (only the listed rows cross PCIe)
+skmp_status dims_rows(const void* T, int64_t ld, int64_t n, int dtype, std::vector<int64_t> rows, int64_t t_star,
+                      int m, int ex, double* d_score, int64_t* d_nn, Temps& tmp) {
+  const int64_t nrows = (int64_t)rows.size();
+  const void* Tdev = T;
+  int64_t ldd = ld;
+  if (!is_device_ptr(T)) {
+    const size_t es = elem_size(dtype);
+    char* d = nullptr;
+    SKMP_CUDA(tmp.alloc(&d, (size_t)nrows * (size_t)n * es, staging_pool()));
+    for (int64_t q = 0; q < nrows; ++q) {
+      SKMP_CUDA(cudaMemcpyAsync(d + (size_t)q * n * es, static_cast<const char*>(T) + (size_t)rows[(size_t)q] * ld * es,
+                                (size_t)n * es, cudaMemcpyHostToDevice, tmp.st));
+      rows[(size_t)q] = q;
+    }
+    Tdev = d;
+    ldd = n;
+  }
+  int64_t* d_rows;
+  skmp_status s;
+  if ((s = upload(rows, &d_rows, tmp)) != SKMP_OK) return s;
+  char* ws;
+  SKMP_CUDA(tmp.alloc(&ws, dims_ws_bytes(nrows, n, m)));
+  SKMP_CUDA(launch_dims(Tdev, ldd, n, dtype, d_rows, nrows, t_star, m, ex, d_score, d_nn, ws, tmp.st));
+  return SKMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 // ============================================================================================
 // detection
 // ============================================================================================
@@ -1309,61 +1407,114 @@ skmp_status discord_dims(const void* T, int64_t ld, int64_t n, int32_t dtype, co
   if (!T || !rows || !scores || !j_star) return set_error(SKMP_E_INVALID_ARG, "discord_dims: NULL argument");
   if (dtype != SKMP_F32 && dtype != SKMP_F64) return set_error(SKMP_E_INVALID_ARG, "discord_dims: bad dtype");
   if (nrows < 1 || m < 2 || ld < n) return set_error(SKMP_E_INVALID_ARG, "discord_dims: need nrows >= 1, m >= 2, ld >= n");
-  if (n < m) return set_error(SKMP_E_SERIES_TOO_SHORT, "discord_dims: n < m");
-  const int64_t n_sub = n - m + 1;
-  if (t_star < 0 || t_star >= n_sub) return set_error(SKMP_E_INVALID_ARG, "discord_dims: t_star outside [0, n-m+1)", t_star);
-  const int ex = excl < 0 ? (m + 1) / 2 : excl;
-  if (t_star - ex - 1 < 0 && t_star + ex + 1 >= n_sub)
-    return set_error(SKMP_E_NO_ADMISSIBLE, "discord_dims: no window farther than excl from t_star");
-  int64_t maxrow = 0;
-  for (int64_t q = 0; q < nrows; ++q) {
-    if (rows[q] < 0) return set_error(SKMP_E_INVALID_ARG, "discord_dims: negative stream row", q);
-    maxrow = std::max(maxrow, rows[q]);
-  }
-  skmp_status s = require_device();
+  int ex = 0;
+  skmp_status s = dims_validate("discord_dims", n, t_star, m, excl, &ex);
   if (s) return s;
+  for (int64_t q = 0; q < nrows; ++q)
+    if (rows[q] < 0) return set_error(SKMP_E_INVALID_ARG, "discord_dims: negative stream row", q);
+  if ((s = require_device()) != SKMP_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Temps tmp(st);
-  const void* Tdev;
-  int64_t ldd;
-  std::vector<int64_t> hrows(rows, rows + nrows);
-  if (is_device_ptr(T)) {
-    Tdev = T;
-    ldd = ld;
-  } else {  // host streams: stage only the listed rows (compacted), not the whole matrix
-    const size_t es = elem_size(dtype);
-    char* d = nullptr;
-    SKMP_CUDA(tmp.alloc(&d, (size_t)nrows * (size_t)n * es));
-    for (int64_t q = 0; q < nrows; ++q) {
-      SKMP_CUDA(cudaMemcpyAsync(d + (size_t)q * n * es, static_cast<const char*>(T) + (size_t)rows[q] * ld * es,
-                                (size_t)n * es, cudaMemcpyHostToDevice, st));
-      hrows[(size_t)q] = q;
-    }
-    Tdev = d;
-    ldd = n;
-  }
-  (void)maxrow;
-  int64_t* d_rows;
-  if ((s = upload(hrows, &d_rows, tmp)) != SKMP_OK) return s;
   double* d_score;
   int64_t* d_nn;
-  char* ws;
   SKMP_CUDA(tmp.alloc(&d_score, (size_t)nrows));
   SKMP_CUDA(tmp.alloc(&d_nn, (size_t)nrows));
-  SKMP_CUDA(tmp.alloc(&ws, dims_ws_bytes(nrows, n, m)));
-  SKMP_CUDA(launch_dims(Tdev, ldd, n, dtype, d_rows, nrows, t_star, m, ex, d_score, d_nn, ws, st));
+  if ((s = dims_rows(T, ld, n, dtype, std::vector<int64_t>(rows, rows + nrows), t_star, m, ex, d_score, d_nn,
+                     tmp)) != SKMP_OK)
+    return s;
   std::vector<double> hs((size_t)nrows);
   std::vector<int64_t> hn((size_t)nrows);
   SKMP_CUDA(cudaMemcpyAsync(hs.data(), d_score, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
   SKMP_CUDA(cudaMemcpyAsync(hn.data(), d_nn, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
   SKMP_CUDA(cudaStreamSynchronize(st));
-  // Alg. 3 lines 3-7: strict '>' over the group in order (reading 20: from -inf)
-  int64_t best = -1;
-  for (int64_t q = 0; q < nrows; ++q)
-    if (best < 0 || hs[(size_t)q] > hs[(size_t)best]) best = q;
   memcpy(scores, hs.data(), sizeof(double) * nrows);
   if (nn) memcpy(nn, hn.data(), sizeof(int64_t) * nrows);
-  *j_star = best;
+  *j_star = first_strict_max(hs);
+  return ok();
+}
+
+skmp_status discord_dims_group(const skmp_sketch* h, int32_t g, const skmp_source* src, int32_t nsrc,
+                               int64_t t_star, int32_t m, int32_t excl, skmp_dim_result* out, void* stream) {
+  if (!h || !out || (nsrc > 0 && !src) || nsrc < 0)
+    return set_error(SKMP_E_INVALID_ARG, "discord_dims_group: NULL argument or nsrc < 0");
+  const bool dense = h->proj == SKMP_PROJ_DENSE;
+  if (!dense && (g < 0 || g >= h->k)) return set_error(SKMP_E_INVALID_ARG, "discord_dims_group: group outside [0, k)", g);
+  if (m < 2) return set_error(SKMP_E_INVALID_ARG, "discord_dims_group: m < 2");
+  int ex = 0;
+  skmp_status s = dims_validate("discord_dims_group", h->n, t_star, m, excl, &ex);
+  if (s) return s;
+  // where each stream id lives: the first source listing it
+  std::unordered_map<uint64_t, std::pair<int32_t, int64_t>> where;
+  for (int32_t q = 0; q < nsrc; ++q) {
+    const skmp_source& x = src[q];
+    if (x.rows < 0 || (x.rows > 0 && (!x.T || !x.ids)) || (x.rows > 0 && x.ld < h->n))
+      return set_error(SKMP_E_INVALID_ARG, "discord_dims_group: source needs T, ids and ld >= n", q);
+    for (int64_t r = 0; r < x.rows; ++r) where.emplace(x.ids[r], std::make_pair(q, r));
+  }
+  // J_g in the plan's order (Alg. 3 scans the group's members in order); members
+  // held by no source are skipped (a rank scores only its own streams)
+  std::vector<std::vector<int64_t>> rows((size_t)nsrc);
+  std::vector<std::vector<int64_t>> slot((size_t)nsrc);
+  std::vector<uint64_t> member_id;
+  for (size_t p = 0; p < h->ids.size(); ++p) {
+    if (!dense && h->g[p] != g) continue;
+    auto it = where.find(h->ids[p]);
+    if (it == where.end()) continue;
+    rows[(size_t)it->second.first].push_back(it->second.second);
+    slot[(size_t)it->second.first].push_back((int64_t)member_id.size());
+    member_id.push_back(h->ids[p]);
+  }
+  const int64_t nm = (int64_t)member_id.size();
+  out->n_scored = nm;
+  if (nm == 0) return ok();
+  if ((s = require_device()) != SKMP_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Temps tmp(st);
+  double* d_score;
+  int64_t* d_nn;
+  SKMP_CUDA(tmp.alloc(&d_score, (size_t)nm));
+  SKMP_CUDA(tmp.alloc(&d_nn, (size_t)nm));
+  std::vector<int64_t> base((size_t)nsrc + 1, 0);
+  for (int32_t q = 0; q < nsrc; ++q) base[(size_t)q + 1] = base[(size_t)q] + (int64_t)rows[(size_t)q].size();
+  for (int32_t q = 0; q < nsrc; ++q) {
+    if (rows[(size_t)q].empty()) continue;
+    if ((s = dims_rows(src[q].T, src[q].ld, h->n, h->dtype, rows[(size_t)q], t_star, m, ex, d_score + base[(size_t)q],
+                       d_nn + base[(size_t)q], tmp)) != SKMP_OK)
+      return s;
+  }
+  std::vector<double> hs((size_t)nm);
+  std::vector<int64_t> hn((size_t)nm);
+  SKMP_CUDA(cudaMemcpyAsync(hs.data(), d_score, sizeof(double) * nm, cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaMemcpyAsync(hn.data(), d_nn, sizeof(int64_t) * nm, cudaMemcpyDeviceToHost, st));
+  SKMP_CUDA(cudaStreamSynchronize(st));
+  // back to member (plan) order, then the first strict maximiser
+  std::vector<double> ms((size_t)nm);
+  std::vector<int64_t> mn((size_t)nm);
+  for (int32_t q = 0; q < nsrc; ++q)
+    for (size_t r = 0; r < rows[(size_t)q].size(); ++r) {
+      ms[(size_t)slot[(size_t)q][r]] = hs[(size_t)(base[(size_t)q] + (int64_t)r)];
+      mn[(size_t)slot[(size_t)q][r]] = hn[(size_t)(base[(size_t)q] + (int64_t)r)];
+    }
+  const int64_t b = first_strict_max(ms);
+  out->score = ms[(size_t)b];
+  out->id = member_id[(size_t)b];
+  out->nn = mn[(size_t)b];
+  return ok();
+}
+
+skmp_status discord_dims_merge(const skmp_dim_result* parts, int32_t nparts, skmp_dim_result* out) {
+  if (!parts || !out || nparts < 1) return set_error(SKMP_E_INVALID_ARG, "discord_dims_merge: NULL argument or nparts < 1");
+  int32_t best = -1;
+  int64_t total = 0;
+  for (int32_t q = 0; q < nparts; ++q) {
+    if (parts[q].n_scored < 0) return set_error(SKMP_E_INVALID_ARG, "discord_dims_merge: negative n_scored", q);
+    if (parts[q].n_scored == 0) continue;
+    total += parts[q].n_scored;
+    // parts come in J_g order (contiguous id shards in rank order): strict '>' keeps the first
+    if (best < 0 || parts[q].score > parts[best].score) best = q;
+  }
+  if (best >= 0) *out = parts[best];
+  out->n_scored = total;
   return ok();
 }
 

@@ -63,7 +63,7 @@ const Nccl& nccl() {
 }
 
 skmp_status nccl_error(ncclResult_t r, const char* where) {
-  return set_error(SKMP_E_CUDA, std::string(where) + ": NCCL " + nccl().error_string(r), -1);
+  return set_error(SKMP_E_NCCL, std::string(where) + ": NCCL " + nccl().error_string(r), -1);
 }
 #define SKMP_NCCL(call)                                          \
   do {                                                           \
@@ -73,7 +73,7 @@ skmp_status nccl_error(ncclResult_t r, const char* where) {
 
 skmp_status need_nccl() {
   const Nccl& n = nccl();
-  return n.ok ? SKMP_OK : set_error(SKMP_E_CUDA, n.why, -1);
+  return n.ok ? SKMP_OK : set_error(SKMP_E_NCCL, n.why, -1);
 }
 
 // FP64 keys {value, index} -> separate value / index arrays and back (NCCL reduces contiguous
@@ -183,7 +183,7 @@ skmp_status mp_selfjoin_dist(skmp_comm* comm, const void* R, int32_t k, int64_t 
     if (r != ncclSuccess) return fail(nccl_error(r, "ncclAllReduce(keys)"));
   } else {
     const int64_t ne = count / 2;
-    cudaError_t e = cudaMallocAsync((void**)&tmp, sizeof(int64_t) * 2 * (size_t)ne, st);
+    cudaError_t e = dmalloc((void**)&tmp, sizeof(int64_t) * 2 * (size_t)ne, st);
     if (e != cudaSuccess) return fail(cuda_error(e, "mp_selfjoin_dist: key buffers"));
     int64_t *v = tmp, *x = tmp + ne;
     const unsigned blocks = (unsigned)std::min<int64_t>((ne + 255) / 256, 148 * 16);

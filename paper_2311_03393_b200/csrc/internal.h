@@ -10,6 +10,11 @@
 
 namespace skmp {
 
+// Device allocation from the library's own stream-ordered WORK pool (api.cu); freed with
+// cudaFreeAsync.  Every library allocation goes through it (or the staging pool), never the
+// process's default pool.
+cudaError_t dmalloc(void** p, size_t bytes, cudaStream_t st);
+
 // ------------------------------------------------------------------------------------------
 // error plumbing
 // ------------------------------------------------------------------------------------------

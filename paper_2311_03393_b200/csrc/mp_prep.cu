@@ -197,7 +197,7 @@ cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream
   for (int g = 0; g < w.k; ++g) nser += h_nflat[g] > 0;
   if (nser == 0) return cudaSuccess;
   int32_t* d_ids = nullptr;
-  cudaError_t e = cudaMallocAsync(&d_ids, sizeof(int32_t) * nser, st);
+  cudaError_t e = dmalloc((void**)&d_ids, sizeof(int32_t) * nser, st);
   if (e) return e;
   int32_t* h_ids = nullptr;
   e = cudaMallocHost(&h_ids, sizeof(int32_t) * nser);

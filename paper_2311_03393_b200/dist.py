@@ -11,8 +11,9 @@ the ranks holding that value), after which any rank can finalize.
 AB-join: the same scheme over its two passes taken as one diagonal sequence (mp_abband); the
 keys of both sides are max-all-reduced and each side's windows are finalized in row slices.
 
-Only the collectives live here (torch.distributed: NCCL on GPUs, gloo in the CPU tests);
-every computation step is a C-ABI call into libsketchmp.so.
+Only the collectives live here (torch.distributed: NCCL on GPUs, gloo in the CPU tests and in
+the one-GPU multi-rank test, where CUDA tensors are staged through host memory around each
+collective); every computation step is a C-ABI call into libsketchmp.so.
 """
 from __future__ import annotations
 
@@ -21,11 +22,51 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (F32, F64, Sketch, detect_dimension, mp_abband, mp_band, mp_create, mp_create_ab, mp_finalize,
-               mp_finalize_ab, mp_finalize_rows, mp_join, mp_join_ab, mp_keys, mp_tile_width, sketch_refresh,
+from . import (F32, F64, DimResult, Sketch, discord_dims_group, discord_dims_merge, mp_abband, mp_band,
+               mp_create, mp_create_ab, mp_finalize, mp_finalize_ab, mp_finalize_rows, mp_join, mp_join_ab, mp_keys, mp_tile_width, sketch_refresh,
                sketch_view64)
 
 INT64_MIN = -(1 << 63)
+
+
+def _staged(t: torch.Tensor, group) -> bool:
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def all_reduce(t: torch.Tensor, op=dist.ReduceOp.SUM, group=None) -> None:
+    """dist.all_reduce in place; CUDA tensors go through host memory under gloo."""
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def reduce(t: torch.Tensor, dst: int, op=dist.ReduceOp.SUM, group=None) -> None:
+    if _staged(t, group):
+        h = t.cpu()
+        dist.reduce(h, dst, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.reduce(t, dst, op=op, group=group)
+
+
+def broadcast(t: torch.Tensor, src: int, group=None) -> None:
+    if _staged(t, group):
+        h = t.cpu()
+        dist.broadcast(h, src, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src, group=group)
+
+
+def all_gather(t: torch.Tensor, group=None) -> list[torch.Tensor]:
+    world = dist.get_world_size(group)
+    src = t.cpu() if _staged(t, group) else t
+    out = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(out, src, group=group)
+    return out
 
 
 def shard(ids, rank: int, world: int):
@@ -50,7 +91,7 @@ def rank_diagonals(n_sub: int, excl: int, dtype: int, world: int, rank: int) -> 
 def allreduce_sketch(sk: Sketch, group=None) -> None:
     """Sum the per-rank partial FP64 sketches in place and refresh the dtype copy."""
     R64 = sketch_view64(sk)
-    dist.all_reduce(R64, op=dist.ReduceOp.SUM, group=group)
+    all_reduce(R64, op=dist.ReduceOp.SUM, group=group)
     sketch_refresh(sk)
 
 
@@ -58,14 +99,14 @@ def reduce_keys(keys: torch.Tensor, words: int, group=None) -> None:
     """In-place max-reduce of profile keys across ranks (the NCCL min-with-index reduce of
     SURVEY §8(e), expressed on the library's larger-is-better key words)."""
     if words == 1:
-        dist.all_reduce(keys, op=dist.ReduceOp.MAX, group=group)
+        all_reduce(keys, op=dist.ReduceOp.MAX, group=group)
         return
     kv = keys.view(-1, 2)
     v = kv[:, 0].clone()
-    dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+    all_reduce(v, op=dist.ReduceOp.MAX, group=group)
     idx = kv[:, 1].clone()
     idx.masked_fill_(kv[:, 0] != v, INT64_MIN)
-    dist.all_reduce(idx, op=dist.ReduceOp.MAX, group=group)
+    all_reduce(idx, op=dist.ReduceOp.MAX, group=group)
     kv[:, 0].copy_(v)
     kv[:, 1].copy_(idx)
 
@@ -95,26 +136,26 @@ def mp_selfjoin_dist(R: torch.Tensor, m: int, *, excl: int = -1, reseed_rows: in
 
 def detect_dimension_dist(sk: Sketch, sources, t: int, g: int, m: int, device, group=None):
     """Alg. 3 with the streams sharded over ranks (each rank's sketch plan holds its own shard):
-    every rank scores its members of J_g (discord_dims), then the (score, plan order) maxima are
-    all-gathered and every rank returns the same (id*, score, nn).  Ranks hold contiguous id
-    shards, so (rank, local order) is the global plan order of Alg. 3's scan."""
-    return gather_dimension(detect_dimension(sk, sources, t, g, m), device, group)
+    every rank scores its members of J_g (discord_dims_group), then the ranks' winners are
+    all-gathered and merged by the C-ABI (discord_dims_merge: first strict maximum in rank
+    order; ranks hold contiguous id shards, so rank order is J_g's plan order).  Every rank
+    returns the same (id*, score, nn), or None when no rank holds a member of J_g."""
+    return gather_dimension(discord_dims_group(sk, g, sources, t, m), device, group)
 
 
-def gather_dimension(loc, device, group=None):
-    """All-gather every rank's local Alg. 3 winner (id, score, nn) or None and return the global
-    one: the first strict maximum in rank order (ranks hold contiguous id shards)."""
+def gather_dimension(loc: DimResult, device, group=None):
+    """All-gather every rank's DimResult as four exact 64-bit words (score bits, id, nn,
+    n_scored; the id travels as int64 bits, so ids >= 2^53 survive) and merge them in rank
+    order through discord_dims_merge."""
     world = dist.get_world_size(group)
-    row = torch.tensor([-1.0, 0.0, 0.0, 0.0], dtype=torch.float64, device=device) if loc is None else \
-        torch.tensor([1.0, loc[1], float(loc[0]), float(loc[2])], dtype=torch.float64, device=device)
-    allr = [torch.empty_like(row) for _ in range(world)]
-    dist.all_gather(allr, row, group=group)
-    best = None
-    for r in range(world):
-        ok, sc, j, nn = (float(x) for x in allr[r].tolist())
-        if ok > 0 and (best is None or sc > best[1]):  # strict: the earliest rank wins ties
-            best = (int(j), sc, int(nn))
-    return best
+    words = np.array([loc.score], dtype=np.float64).view(np.int64).tolist() + \
+        np.array([loc.id], dtype=np.uint64).view(np.int64).tolist() + [int(loc.nn), int(loc.n_scored)]
+    row = torch.tensor(words, dtype=torch.int64, device=device)
+    h = torch.stack([x.cpu() for x in all_gather(row, group)]).numpy()
+    parts = [DimResult(float(h[r, 0:1].view(np.float64)[0]), int(h[r, 1:2].view(np.uint64)[0]), int(h[r, 2]),
+                       int(h[r, 3])) for r in range(world)]
+    best = discord_dims_merge(parts)
+    return None if best.n_scored == 0 else (int(best.id), float(best.score), int(best.nn))
 
 
 def row_range(n_sub: int, world: int, rank: int) -> tuple[int, int]:
@@ -131,8 +172,8 @@ def finalize_dist(w, group=None, dst: int = 0):
     rank = dist.get_rank(group)
     lo, hi = row_range(w.n_sub, world, rank)
     P, I, inert = mp_finalize_rows(w, lo, hi)
-    dist.reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
-    dist.reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
+    reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
+    reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
     return (P, I, inert) if rank == dst else None
 
 
@@ -163,8 +204,8 @@ def mp_abjoin_dist(RA: torch.Tensor, RB: torch.Tensor, m: int, *, reseed_rows: i
         if hi == 0:
             lo = hi = w.n_sub   # empty slice ((0, 0) would mean all windows)
         P, I, inert = mp_finalize_ab(w, o, lo, hi)
-        dist.reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
-        dist.reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
+        reduce(P, dst, op=dist.ReduceOp.SUM, group=group)
+        reduce(I, dst, op=dist.ReduceOp.SUM, group=group)
         out += [P, I]
     a.free()
     b.free()

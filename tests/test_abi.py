@@ -42,7 +42,9 @@ def test_status_strings():
 @pytest.mark.parametrize("k,seed", [(1, 0), (7, 2311033932), (64, 12345), (100, 2**63 + 5)])
 def test_hash_plan_matches_oracle(k, seed):
     """C++ Carter-Wegman plan (128-bit products) == the oracle's Python-integer plan, bit-equal."""
-    ids = np.concatenate([np.arange(0, 3000), np.array([2**61 - 2, 2**61 - 1, 2**61, 2**64 - 1], dtype=np.uint64)]).astype(np.uint64)
+    edge = [2**61 - 2, 2**61 - 1, 2**61, 2**61 + 1, 2**62, 2**63, 2**64 - 2, 2**64 - 1]
+    ids = np.concatenate([np.arange(0, 3000, dtype=np.uint64), np.array(edge, dtype=np.uint64)])
+    assert ids.dtype == np.uint64 and [int(x) for x in ids[3000:]] == edge   # no float promotion
     g, s = skmp.sketch_hash_plan(ids, k, seed)
     go, so = plan_count_sketch([int(x) for x in ids], k, seed)
     assert np.array_equal(g, np.array(go, dtype=np.int32))
@@ -244,3 +246,35 @@ def test_native_comm_argument_validation():
     cfg = skmp._mpcfg(16)
     assert L.mp_selfjoin_dist(None, None, 1, 100, 100, 0, ctypes.byref(cfg), None, None, None, None) == 1
     L.skmp_comm_free(None)
+
+
+def test_dims_merge_host_only():
+    """discord_dims_merge (host-only): the first strict maximum over parts in J_g order; parts
+    with nothing scored are skipped; ids keep all 64 bits."""
+    D = skmp.DimResult
+    r = skmp.discord_dims_merge([D(1.0, 7, 3, 2), D(2.0, 2**64 - 1, 9, 4), D(2.0, 5, 1, 1), D(9.0, 3, 3, 0)])
+    assert (r.score, r.id, r.nn, r.n_scored) == (2.0, 2**64 - 1, 9, 7)
+    r = skmp.discord_dims_merge([D(0.0, 0, 0, 0), D(0.0, 0, 0, 0)])
+    assert r.n_scored == 0
+    L = skmp.lib()
+    assert L.discord_dims_merge(None, 1, None) == 1
+    parts = (D * 1)(D(1.0, 1, 1, -1))
+    out = D()
+    assert L.discord_dims_merge(ctypes.cast(parts, ctypes.c_void_p), 1, ctypes.byref(out)) == 1
+
+
+def test_dims_group_argument_validation():
+    """discord_dims_group rejects a NULL handle / output before any device work."""
+    L = skmp.lib()
+    out = skmp.DimResult()
+    assert L.discord_dims_group(None, 0, None, 0, 0, 16, -1, ctypes.byref(out), None) == 1
+    assert L.discord_dims_group(None, 0, None, -1, 0, 16, -1, None, None) == 1
+
+
+def test_trim_and_free_without_gpu():
+    """skmp_trim is callable without a device (no pools yet: a no-op); sketch_free[_async] of
+    NULL is a no-op."""
+    skmp.skmp_trim()
+    L = skmp.lib()
+    L.sketch_free(None)
+    L.sketch_free_async(None, None)

@@ -146,9 +146,14 @@ def _worker(rank, world, port, q):
         dist.reduce(Is, 0, op=dist.ReduceOp.SUM)
         out["fin"] = (Ps.numpy(), Is.numpy(), (lo, hi))
         # ---- Alg. 3 across ranks: global first strict maximum in rank order --------------
-        locs = [(11, 2.5, 40), (23, 2.5, 7)]          # a tie: rank 0 must win
+        D = skmp.DimResult
+        locs = [D(2.5, 11, 40, 3), D(2.5, 23, 7, 2)]          # a tie: rank 0 must win
         out["dim_tie"] = sdist.gather_dimension(locs[rank], "cpu")
-        out["dim_none"] = sdist.gather_dimension(None if rank == 0 else (5, 1.0, 3), "cpu")
+        out["dim_none"] = sdist.gather_dimension(D(0.0, 0, 0, 0) if rank == 0 else D(1.0, 5, 3, 4), "cpu")
+        # ids >= 2^53 (64-bit keyed names) must cross ranks exactly (no float64 rounding)
+        big = [D(1.5, 2**64 - 3, 9, 1), D(2.0, 2**53 + 1, 8, 1)]
+        out["dim_big"] = sdist.gather_dimension(big[rank], "cpu")
+        out["dim_empty"] = sdist.gather_dimension(D(0.0, 0, 0, 0), "cpu")
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -210,6 +215,8 @@ def test_two_rank_bands_and_reductions():
     for rank in range(world):
         assert res[rank]["dim_tie"] == (11, 2.5, 40)
         assert res[rank]["dim_none"] == (5, 1.0, 3)
+        assert res[rank]["dim_big"] == (2**53 + 1, 2.0, 8)
+        assert res[rank]["dim_empty"] is None
     cfg = synthgen.scaled(synthgen.CONFIGS["c2"], d=9, n=600, k=3)
     T = synthgen.streams(cfg)
     g, s = plan_count_sketch(np.arange(cfg.d), cfg.k, cfg.seed)

@@ -46,6 +46,40 @@ def test_discord_topk_parity(cuda, dtype, k, n_sub, top, radius):
     assert [d.score for d in got] == [s for *_, s in want]
 
 
+@pytest.mark.parametrize("dtype,k,n_sub,top,radius", [
+    ("f32", 64, 2_000_000, 64, 128),     # > 296 CTAs x 256 windows: the grid-stride argmax path
+    ("f32", 32, 1_999_745, 100, 128),    # C5's shape and bench.py's top-100
+    ("f64", 16, 1_000_003, 40, 77),      # ragged, odd radius
+])
+def test_discord_topk_parity_grid_stride(cuda, dtype, k, n_sub, top, radius):
+    """discord_topk above 296 x 256 = 75,776 windows (detect.cu's capped grid walks the profile
+    with a grid stride) against the oracle's combine + greedy top-K (Alg. 2; the
+    ordered list of P:L445), with exact ties across groups, within a group and at the maxima."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    rng = np.random.default_rng([n_sub, k, 0x70B])
+    P = rng.uniform(0.5, 6.0, size=(k, n_sub)).astype(np.float32 if dtype == "f32" else np.float64)
+    # exact ties at the top: plateaus of equal maxima far apart, across groups, and repeated
+    # values inside one mask radius (the smallest index must win every time)
+    for q, t in enumerate(rng.choice(n_sub, size=3 * top, replace=False)):
+        P[q % k, t] = 7.0 + (q % 5) * 0.25
+    P[:, n_sub // 2] = 9.0
+    P[3, n_sub - 1] = 9.0
+    P[5, 0] = 9.0
+    I = rng.integers(0, n_sub, size=(k, n_sub))
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    Pt = torch.from_numpy(P).to(cuda, tdt)
+    It = torch.from_numpy(I).to(cuda)
+    inert = np.zeros(k, dtype=bool)
+    inert[1] = True
+    got = skmp.discord_topk(Pt, It, inert, m=2 * radius, top=top, radius=radius)
+    C, G = ref.combine(P.astype(np.float64), inert)
+    want = ref.topk_greedy(C, G, I, top, radius)
+    assert len(got) == len(want) == top
+    assert [(d.t, d.g, d.nn) for d in got] == [(t, g, nn) for t, g, nn, _ in want]
+    assert [d.score for d in got] == [s for *_, s in want]
+
+
 def test_discord_topk_all_inert(cuda):
     import torch
     import paper_2311_03393_b200 as skmp

@@ -2,14 +2,23 @@
 outputs the oracle computes one by one (SURVEY §8(c) "Parity contract"):
 
 * C3 (d=1000, n=1e5, FP32): sketch at sampled time columns; profile at sampled rows of every
-  series by brute force, and EVERY row of every series against the tier-B reference; every
-  reported discord's score re-derived by the oracle;
+  series by brute force, and EVERY row of every series against the tier-B reference; the GPU's
+  top-20 discords against the oracle's combine + greedy top-K over those tier-B profiles
+  (identical (t, g) lists up to documented ties);
 * C4 (d=10,000, n=2e5, FP32) dynamic test: build, add 500, delete 500 (the bench step) -> the
-  sketch at sampled columns equals the oracle's sketch of the final stream set; sampled rows,
-  and every row of 4 of the 64 series against the tier-B reference;
-* C5-shaped join (k=32, n=2e6, m=256, FP32): sampled rows, and bit-identical keys for a 2-band
-  split (the multi-GPU decomposition).
-The oracle always works on its own sketch of the generator's streams (never on GPU output)."""
+  sketch at sampled columns equals the oracle's sketch of the final stream set; 16 brute-force
+  rows per series plus every reported discord's row; every row of 4 of the 64 series against
+  the tier-B reference; the top-40 against the oracle's greedy top-K on the checked profile
+  (the full 64-series tier-B top-K comparison is tools/full_parity.py --config c4);
+* C5 (d=2,000, n=2e6, m=256, k=32, FP32), bench.py's headline workload end to end: its own
+  seasonal streams -> sketch_build -> mp_selfjoin -> discord_topk(100): the sketch at sampled
+  columns vs Alg. 1, 16 brute-force rows per series plus every reported discord's row, the
+  top-100 against the oracle's greedy top-K on the checked profile;
+* C5-shaped join (k=32, n=2e6, m=256, FP32): bit-identical keys for a 2-band split (the
+  multi-GPU decomposition).
+The oracle always works on its own sketch of the generator's streams (never on GPU output),
+except that the top-K step is also checked on its own (oracle greedy over the GPU profile that
+the row checks just validated) where no full oracle profile exists."""
 from __future__ import annotations
 
 import math
@@ -20,6 +29,7 @@ import pytest
 import synthgen
 from oracle import reference as ref
 from oracle.hashplan import plan_count_sketch
+from tests._parity import check_topk
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -82,8 +92,10 @@ def _check_full_tierb(R_or, P, I, m, series, tol=1e-3, label=""):
     excl = (m + 1) // 2
     floor = 1e-3 * math.sqrt(m)
     ties = 0
+    out = {}
     for g in series:
         Pt, It = ref.selfjoin_tierb(R_or[g], m, excl)
+        out[g] = (Pt, It)
         err = np.abs(P[g] - Pt) / np.maximum(Pt, floor)
         assert err.max() <= tol, f"{label} g={g}: rel err {err.max():.2e} at row {int(np.argmax(err))}"
         mism = np.where(I[g] != It)[0]
@@ -98,6 +110,23 @@ def _check_full_tierb(R_or, P, I, m, series, tol=1e-3, label=""):
                 assert d <= Pt[i] * (1 + tol) + floor * tol, (label, g, i, j, It[i], d, Pt[i])
         ties += len(mism)
     print(f"{label}: full profiles of {len(series)} series vs tier B, {ties} documented ties")
+    return out
+
+
+def _check_topk_on_gpu_profile(top, Pn, In, inert, m, label):
+    """The top-K step alone at full size: the oracle's combine + greedy top-K (Alg. 2, P:L249-269;
+    P:L445) over the GPU profile gives the GPU's list exactly (same values in, so no tolerance)."""
+    C, G = ref.combine(Pn.astype(np.float64), inert)
+    want = ref.topk_greedy(C, G, In, len(top), (m + 1) // 2)
+    assert [(d.t, d.g, d.nn) for d in top] == [(t, g, nn) for t, g, nn, _ in want], label
+    assert [d.score for d in top] == [sc for *_, sc in want], label
+
+
+def _discord_rows(top):
+    extra = {}
+    for d in top:
+        extra.setdefault(d.g, []).append(d.t)
+    return {k_: np.array(v) for k_, v in extra.items()}
 
 
 def test_c3_full(cuda):
@@ -122,7 +151,18 @@ def test_c3_full(cuda):
     for d in top:
         extra.setdefault(d.g, []).append(d.t)
     _check_rows(R_or, Pn, In, cfg.m, 3, seed=33, extra_rows={k_: np.array(v) for k_, v in extra.items()})
-    _check_full_tierb(R_or, Pn, In, cfg.m, range(cfg.k), label="C3")   # all 32 x 99,873 rows
+    tb = _check_full_tierb(R_or, Pn, In, cfg.m, range(cfg.k), label="C3")   # all 32 x 99,873 rows
+    # identical top-K discord locations (north_star): the oracle's own combined profile (tier-B
+    # profiles of its own sketch), Alg. 2 combine + greedy top-20, vs the GPU's list
+    inert_or = ref.inert_groups([ref.window_stats(R_or[gg], cfg.m)[2] for gg in range(cfg.k)])
+    assert np.array_equal(inert, inert_or)
+    P_or = np.stack([tb[gg][0] for gg in range(cfg.k)])
+    I_or = np.stack([tb[gg][1] for gg in range(cfg.k)])
+    C_or, G_or = ref.combine(P_or, inert_or)
+    want = ref.topk_greedy(C_or, G_or, I_or, 20, cfg.excl)
+    ties = check_topk(top, want, C_or, 1e-3, label="C3 top-20")
+    print(f"C3 top-20 vs the oracle: {20 - ties} identical, {ties} documented ties")
+    _check_topk_on_gpu_profile(top, Pn, In, inert, cfg.m, "C3")
     for d in top:  # reported scores are the profile values, and the oracle agrees
         assert d.score == float(Pn[d.g, d.t])
         assert d.score == max(float(Pn[gg, d.t]) for gg in range(cfg.k) if not inert[gg])
@@ -143,6 +183,7 @@ def test_c4_dynamic_full(cuda):
     skmp.sketch_add_dim(sk, torch.from_numpy(Ta).to(cuda), add_ids)
     skmp.sketch_del_dim(sk, Td[del_ids.astype(np.int64)].contiguous(), del_ids)
     P, I, inert = skmp.mp_selfjoin(sk.R, cfg.m)
+    top = skmp.discord_topk(P, I, inert, m=cfg.m, top=40)
     torch.cuda.synchronize()
     keep = np.setdiff1d(np.arange(cfg.d), del_ids.astype(np.int64))
     final_T = np.concatenate([T[keep], Ta])
@@ -158,8 +199,9 @@ def test_c4_dynamic_full(cuda):
     assert sorted(plan["ids"].tolist()) == sorted(final_ids.tolist())
     R_or = _oracle_sketch_full(final_T, mu, sg, g, s, cfg.k)
     Pn, In = P.cpu().numpy(), I.cpu().numpy()
-    _check_rows(R_or, Pn, In, cfg.m, 1, seed=44)
+    _check_rows(R_or, Pn, In, cfg.m, 16, seed=44, extra_rows=_discord_rows(top))
     _check_full_tierb(R_or, Pn, In, cfg.m, (0, 21, 42, 63), label="C4")  # every row of 4 series
+    _check_topk_on_gpu_profile(top, Pn, In, inert, cfg.m, "C4")
 
 
 def test_c5_shape_join_and_bands(cuda):
@@ -192,3 +234,48 @@ def test_c5_shape_join_and_bands(cuda):
         Po, Io, _ = ref.selfjoin_rows(Rh[g], m, excl, rows=rows)
         err = np.abs(Pn[g, rows] - Po) / np.maximum(Po, 1e-3 * math.sqrt(m))
         assert err.max() <= 1e-3, err
+
+
+def test_c5_end_to_end(cuda):
+    """bench.py's headline workload C5 through its own pipeline: the seasonal-plus-noise streams
+    (synthgen.streams_torch, generated on the device: 16 GB) -> sketch_build (Alg. 1) ->
+    mp_selfjoin (Def. 6) -> discord_topk (Alg. 2 + ordered top-100).  The oracle builds its own
+    FP64 sketch from the same streams (copied to the host block by block) and checks the GPU sketch
+    at 32 sampled columns, 16 brute-force rows of every series plus every reported discord's row,
+    and the top-K step on the validated profile."""
+    import torch
+    import paper_2311_03393_b200 as skmp
+    cfg = synthgen.CONFIGS["c5"]
+    k, n, m = cfg.k, cfg.n, cfg.m
+    ids = synthgen.stream_ids(cfg)
+    T = synthgen.streams_torch(cfg, cuda)
+    sk = skmp.sketch_build(T, ids, k, seed=cfg.seed)
+    P, I, inert = skmp.mp_selfjoin(sk.R, m)
+    top = skmp.discord_topk(P, I, inert, m=m, top=2 * cfg.n_discords)
+    torch.cuda.synchronize()
+    assert len(top) == 2 * cfg.n_discords and not inert.any()
+    # the oracle's own sketch (Alg. 1, P:L224-233): two-pass FP64 stream statistics, then the
+    # sequential ascending-j sum per group; B = sum of |terms| at the sampled columns (tolerance)
+    g, s = plan_count_sketch(ids, k, cfg.seed)
+    cols = np.random.default_rng(55).choice(n, 32, replace=False)
+    R_or = np.zeros((k, n))
+    B = np.zeros((k, len(cols)))
+    for j0 in range(0, cfg.d, 50):
+        blk = T[j0:j0 + 50].cpu().numpy()
+        mu, sg = _oracle_stats(blk)
+        for q in range(blk.shape[0]):
+            j = j0 + q
+            z = (blk[q].astype(np.float64) - mu[q]) / sg[q]
+            R_or[g[j]] += s[j] * z
+            B[g[j]] += np.abs(z[cols])
+    del T
+    R64 = sk.R64[:, torch.from_numpy(cols).to(cuda)].cpu().numpy()
+    assert np.all(np.abs(R64 - R_or[:, cols]) <= 1e-12 * B)
+    Rd = sk.R[:, torch.from_numpy(cols).to(cuda)].cpu().numpy()
+    assert np.array_equal(Rd, R64.astype(np.float32))   # one rounding of the FP64 sum
+    sk.free()
+    Pn, In = P.cpu().numpy(), I.cpu().numpy()
+    _check_rows(R_or, Pn, In, m, 16, seed=56, extra_rows=_discord_rows(top))
+    _check_topk_on_gpu_profile(top, Pn, In, inert, m, "C5")
+    hits = sum(1 for q in synthgen.injections(cfg) if any(abs(d.t - q.t) < m for d in top))
+    print(f"C5: {hits}/{len(synthgen.injections(cfg))} injected discords within the top-{len(top)}")

@@ -66,7 +66,8 @@ def test_stream_parity(cuda, dtype, chunks):
             assert dj <= Po[i] + TOL[dtype] * max(Po[i], floor)
     # and the oracle's own end-to-end values (its own sketches)
     err = np.abs(Pg - P_or) / np.maximum(P_or, floor)
-    assert err.max() <= (TOL[dtype] if dtype == "f64" else 5e-3)
+    print(f"stream {dtype} {chunks[:4]}: end-to-end max rel err vs the oracle's own sketches {err.max():.2e}")
+    assert err.max() <= TOL[dtype]
     assert not inert.any()
     # Alg. 2's ranking over the streamed profile
     top = st.topk(5)

@@ -9,7 +9,10 @@ The GPU runs the bench pipeline through the C-ABI (sketch_build, add / delete fo
 mp_selfjoin); the oracle builds its OWN FP64 sketch of the final stream set (Alg. 1) and the
 tier-B FP64 diagonal recurrence (oracle/mp_tierb.c, pinned to the brute force) gives every row's
 profile.  Checks: |P_gpu - P_tierB| <= 1e-3 max(P, 1e-3 sqrt(m)) for EVERY row; an index that
-differs must be a documented tie (the GPU's neighbour as near within the tolerance).  Prints one
+differs must be a documented tie (the GPU's neighbour as near within the tolerance); the GPU's
+top-K discords (discord_topk, K = 2 x injected as bench.py ranks) against the oracle's Alg. 2
+combine + greedy top-K over the tier-B profiles: identical (t, g) lists, a differing entry only
+where the oracle's combined scores of the two candidates agree within the tolerance.  Prints one
 JSON summary line.
 """
 from __future__ import annotations
@@ -54,6 +57,8 @@ def main():
         final_T = np.concatenate([T[keep], Ta])
         final_ids = np.concatenate([ids[keep], add_ids])
     P, I, inert = skmp.mp_selfjoin(sk.R, cfg.m)
+    K = 2 * cfg.n_discords
+    top = skmp.discord_topk(P, I, inert, m=cfg.m, top=K)
     P, I = P.cpu().numpy().astype(np.float64), I.cpu().numpy()
     del Td
     t_gpu = time.time() - t0
@@ -68,8 +73,11 @@ def main():
     floor = 1e-3 * math.sqrt(m)
     worst, ties, rows = 0.0, 0, 0
     t1 = time.time()
+    P_or = np.empty_like(P)
+    I_or = np.empty_like(I)
     for q in range(cfg.k):
         Pt, It = ref.selfjoin_tierb(R_or[q], m, excl)
+        P_or[q], I_or[q] = Pt, It
         err = np.abs(P[q] - Pt) / np.maximum(Pt, floor)
         worst = max(worst, float(err.max()))
         assert err.max() <= args.tol, f"series {q}: rel err {err.max():.3e} at row {int(np.argmax(err))}"
@@ -85,7 +93,19 @@ def main():
                 assert d <= Pt[i] * (1 + args.tol) + floor * args.tol, (q, int(i), j, int(It[i]), d, float(Pt[i]))
         ties += len(mism)
         rows += len(Pt)
+    # identical top-K discord locations (north_star), the oracle's own combined profile
+    inert_or = ref.inert_groups([ref.window_stats(R_or[q], m)[2] for q in range(cfg.k)])
+    assert np.array_equal(inert, inert_or)
+    C_or, G_or = ref.combine(P_or, inert_or)
+    want = ref.topk_greedy(C_or, G_or, I_or, K, excl)
+    assert len(want) == len(top)
+    top_ties = 0
+    for q, (a, b) in enumerate(zip(top, want)):
+        if (a.t, a.g) != (b[0], b[1]):
+            assert abs(C_or[a.t] - C_or[b[0]]) <= args.tol * C_or[b[0]], (q, a, b)
+            top_ties += 1
     print(json.dumps({"config": args.config, "series": cfg.k, "rows_checked": rows, "documented_ties": ties,
+                      "top_k": K, "top_k_identical": K - top_ties, "top_k_documented_ties": top_ties,
                       "max_rel_err": worst, "tolerance": args.tol, "reference": "tier B (oracle/mp_tierb.c)",
                       "gpu_pipeline_s": round(t_gpu, 1), "tierb_s": round(time.time() - t1, 1),
                       "cores": len(os.sched_getaffinity(0))}), flush=True)
