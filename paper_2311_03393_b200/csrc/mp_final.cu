@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -278,6 +279,216 @@ finalize_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* 
   }
 }
 
+// ---- register-resident variant for m <= 32 E (all BASELINE configs: m <= 256) -----------------
+// One warp per row as above, but lane l owns the E consecutive window positions [E l, E l + E):
+// its row values a[e] = R_i[El+e] - mu_i and the candidate values R_o[b + El + t],
+// t < E + SPAN - 1, sit in registers, so the SPAN candidate dot products are E*SPAN register
+// FMAs per lane (the shared-memory variant re-read every operand from shared memory: ~9x the
+// shared traffic).  The windows are staged raw (dtype) in a per-warp shared buffer padded to
+// (E+1)-element groups (conflict-free reads of lane l's group), double-buffered: row r+1's
+// windows are cp.async'ed (its key loaded one row earlier) while row r computes.
+__device__ __forceinline__ void cp_async_b(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+constexpr int kFinRegWarps = 4;  // warps per CTA (~90 registers: 5 CTAs = 20 warps per SM)
+template <int E> __host__ __device__ constexpr int pad_pos(int s) { return s + s / E; }
+template <int E, int SPAN> struct RegBuf {
+  static constexpr int NI = 32 * E;                    // row window positions (>= m)
+  static constexpr int NO = 32 * E + SPAN - 1;         // candidate positions (>= m + SPAN - 1)
+  static constexpr int XI = pad_pos<E>(NI - 1) + 1;
+  static constexpr int XO = pad_pos<E>(NO - 1) + 1;
+  static constexpr int SIZE = XI + XO;                 // elements per buffer
+};
+
+// stage row i's window and the candidate windows of base b (clamped reads: every staged value is
+// a finite series value; the ones past the windows are masked out of the sums)
+template <typename T, int E, int SPAN>
+__device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int64_t n,
+                                          int64_t n_o, int lane) {
+  using B = RegBuf<E, SPAN>;
+  T* xi = buf;
+  T* xo = buf + B::XI;
+  const int32_t ib = (int32_t)i, nn = (int32_t)n, ob = (int32_t)b, no = (int32_t)n_o;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const int s = lane + 32 * q;
+    int32_t idx = ib + s;
+    idx = idx >= nn ? nn - 1 : idx;
+    cp_async_b(xi + pad_pos<E>(s), R + idx, (int)sizeof(T));
+  }
+#pragma unroll
+  for (int q = 0; q < (B::NO + 31) / 32; ++q) {
+    const int t = lane + 32 * q;
+    if (t < B::NO) {
+      int32_t idx = ob + t;
+      idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);
+      cp_async_b(xo + pad_pos<E>(t), Ro + idx, (int)sizeof(T));
+    }
+  }
+}
+
+template <typename T, int SPAN, int E>
+__global__ void __launch_bounds__(32 * kFinRegWarps)
+finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
+                    int64_t* __restrict__ I) {
+  static_assert(SPAN <= 32 && (SPAN & (SPAN - 1)) == 0 && (E % 2) == 0, "geometry");
+  using B = RegBuf<E, SPAN>;
+  __shared__ __align__(16) T fsm[kFinRegWarps * 2 * B::SIZE];
+  const int lane = threadIdx.x & 31;
+  T* buf0 = fsm + (threadIdx.x >> 5) * 2 * B::SIZE;
+  const int64_t i_first = row_lo + ((int64_t)blockIdx.x * kFinRegWarps + (threadIdx.x >> 5)) * kFinRows;
+  const int g = blockIdx.y;
+  const int words = (w.dtype == SKMP_F32) ? 1 : 2;
+  const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
+  const int64_t o = (int64_t)g * w.ldq, oo = (int64_t)g * wo.ldq;
+  const T* R = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
+  const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
+  const int m = w.m;
+  const double sqm = sqrt((double)m);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll), nan = __longlong_as_double(0x7ff8000000000000ll);
+  const int32_t nf = wo.nflat[g];
+  const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
+  auto row_of = [&](int rr) { const int64_t x = i_first + rr; return x < row_hi ? x : row_hi - 1; };
+  auto base_of = [&](int64_t kw) { int64_t kb = 0; return key_arg(kw, words, &kb) ? kb : (int64_t)0; };
+  // prologue: row 0 staged, row 1's key in flight
+  int64_t kw_cur = key_word(keys, row_of(0), words);
+  int64_t kw_nxt = key_word(keys, row_of(1), words);
+  reg_stage<T, E, SPAN>(buf0, R, Ro, row_of(0), base_of(kw_cur), w.n, wo.n, lane);
+  cp_async_commit();
+  for (int rr = 0; rr < kFinRows; ++rr) {
+    const int64_t i_raw = i_first + rr;
+    const bool live = i_raw < row_hi;
+    const int64_t i = row_of(rr);
+    const int64_t kw = kw_cur;
+    T* cur = buf0 + (rr & 1) * B::SIZE;
+    // next row's windows into the other buffer (its key arrived during the previous row), and
+    // the key after it
+    if (rr + 1 < kFinRows)
+      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), base_of(kw_nxt), w.n, wo.n,
+                            lane);
+    cp_async_commit();
+    kw_cur = kw_nxt;
+    kw_nxt = key_word(keys, row_of(rr + 2 < kFinRows ? rr + 2 : kFinRows - 1), words);
+    cp_async_wait1();
+    __syncwarp();
+    const bool fi = w.flat[o + i] != 0;
+    int64_t kb = 0;
+    const bool has = key_arg(kw, words, &kb);
+    const int64_t b = has ? kb : 0;
+    const double mi = w.mu[o + i];
+    // ---- the SPAN candidate dot products, in registers --------------------------------------
+    const T* xi = cur;
+    const T* xo = cur + B::XI;
+    double a[E], wv[E + SPAN - 1];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int s = E * lane + e;
+      a[e] = s < m ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < E + SPAN - 1; ++t) wv[t] = (double)xo[pad_pos<E>(E * lane + t)];
+    double acc[SPAN], asum = 0.0;
+#pragma unroll
+    for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      asum += a[e];
+#pragma unroll
+      for (int d = 0; d < SPAN; ++d) acc[d] = fma(a[e], wv[e + d], acc[d]);
+    }
+#pragma unroll
+    for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+    xsum<SPAN>(acc, lane);
+    int d = xidx<SPAN>(lane);
+    double dd = inf;
+    const int64_t jd = b + d;
+    if (admissible(i, jd, wo.n_sub, excl)) {
+      if (wo.flat[oo + jd]) {
+        dd = (double)m;
+      } else {
+        const double cov = acc[0] - wo.mu[oo + jd] * asum;
+        dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + jd]);
+      }
+    }
+#pragma unroll
+    for (int q = 16; q >= 1; q >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, dd, q);
+      const int oi = __shfl_xor_sync(0xffffffffu, d, q);
+      if (od < dd || (od == dd && oi < d)) {
+        dd = od;
+        d = oi;
+      }
+    }
+    const int64_t jr = dd < inf ? b + d : -1;
+    // ---- the chosen member's distance by explicit differences (Def. 3) ----------------------
+    const bool exact = jr >= 0 && !wo.flat[oo + (jr >= 0 ? jr : 0)];
+    const int64_t je = exact ? jr : (b < 0 ? 0 : (b >= wo.n_sub ? wo.n_sub - 1 : b));
+    const int de = exact ? d : 0;
+    double pe;
+    {
+      const double mj = wo.mu[oo + je];
+      const double ii = 1.0 / w.sig64[o + i], ij = 1.0 / wo.sig64[oo + je];
+      double acc2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int s = E * lane + e;
+        const double zi = __dmul_rn(a[e], ii);
+        const double zj = __dmul_rn((double)xo[pad_pos<E>(s + de)] - mj, ij);
+        const double df = zi - zj;
+        acc2 = s < m ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
+      }
+#pragma unroll
+      for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+      pe = sqrt(acc2);
+    }
+    double p;
+    int64_t j;
+    if (fi) {
+      const int64_t f = smallest_adm_flat(F, nf, i, excl);
+      if (f >= 0) {
+        p = 0.0;
+        j = f;
+      } else {
+        p = sqm;
+        j = (excl < 0 || i - excl - 1 >= 0) ? 0 : i + excl + 1;
+      }
+    } else if (!has) {
+      p = nan;
+      j = -1;
+    } else {
+      j = jr;
+      p = jr < 0 ? nan : (exact ? pe : sqm);
+      if (nf > 0) {
+        const int64_t f = smallest_adm_flat(F, nf, i, excl);
+        if (f >= 0 && (sqm < p || (sqm == p && f < j) || j < 0)) {
+          p = sqm;
+          j = f;
+        }
+      }
+    }
+    if (lane == 0 && live) {
+      P[(int64_t)g * w.n_sub + i] = (T)p;
+      I[(int64_t)g * w.n_sub + i] = j;
+    }
+    __syncwarp();  // this buffer is refilled two rows later
+  }
+}
+
+bool fin_reg_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SKMP_FIN_IMPL");  // "smem": the shared-memory variant (A/B)
+    return !(e && e[0] == 's');
+  }();
+  return on;
+}
+
 }  // namespace
 
 cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* P, int64_t* I,
@@ -289,6 +500,29 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
   const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
 #define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
+#define SKMP_FINR(TT, SP, EE) \
+  finalize_reg_kernel<TT, SP, EE><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
+  const int E = w.m <= 64 ? 2 : (w.m <= 128 ? 4 : (w.m <= 256 ? 8 : 0));
+  if (E > 0 && (w.span == 4 || w.span == 8) && fin_reg_enabled()) {
+    const int64_t perr = (int64_t)kFinRegWarps * kFinRows;
+    grid.x = (unsigned)((row_hi - row_lo + perr - 1) / perr);
+    const int ntr = 32 * kFinRegWarps;
+#undef SKMP_FINR
+#define SKMP_FINR(TT, SP, EE) \
+  finalize_reg_kernel<TT, SP, EE><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
+    if (w.span == 8) {
+      if (E == 2) { if (f32) SKMP_FINR(float, 8, 2); else SKMP_FINR(double, 8, 2); }
+      else if (E == 4) { if (f32) SKMP_FINR(float, 8, 4); else SKMP_FINR(double, 8, 4); }
+      else { if (f32) SKMP_FINR(float, 8, 8); else SKMP_FINR(double, 8, 8); }
+    } else {
+      if (E == 2) { if (f32) SKMP_FINR(float, 4, 2); else SKMP_FINR(double, 4, 2); }
+      else if (E == 4) { if (f32) SKMP_FINR(float, 4, 4); else SKMP_FINR(double, 4, 4); }
+      else { if (f32) SKMP_FINR(float, 4, 8); else SKMP_FINR(double, 4, 8); }
+    }
+    count_launches(1);
+    return cudaGetLastError();
+  }
+#undef SKMP_FINR
   switch (w.span) {
     case 4:
       if (f32) SKMP_FIN(float, 4); else SKMP_FIN(double, 4);
