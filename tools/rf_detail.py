@@ -1,0 +1,40 @@
+"""Per-opcode RF-cycle breakdown (tools/rf_model.py model) of the block starting at an address,
+or with --print the instructions with their cost.  usage: rf_detail.py <cubin> <func> <hexaddr> [--print]"""
+import collections
+import re
+import sys
+
+sys.path.insert(0, __import__("os").path.dirname(__file__))
+import rf_model as M  # noqa: E402
+
+ins = M.sass(sys.argv[1], sys.argv[2])
+addr = int(sys.argv[3], 16)
+bl = [b for b in M.blocks(ins) if b[0][0] == addr][0]
+prev = {}
+cost, cnt = collections.Counter(), collections.Counter()
+for a, x in bl:
+    op, ops = M.parse(x)
+    base = op.split(".")[0]
+    srcs = ops[2:] if base == "FSETP" else ops[1:]
+    even, odd, now = set(), set(), {}
+    for slot, o in enumerate(srcs):
+        m = re.match(r"-?\|?(R\d+)", o)
+        if not m or o.startswith("RZ"):
+            continue
+        r = int(m.group(1)[1:])
+        wide = base in ("FFMA2", "FMUL2") and ".F32x2" in o
+        if ".reuse" in o:
+            now[slot] = r
+        if prev.get(slot) == r:
+            continue
+        for q in ([r, r + 1] if wide else [r]):
+            (even if q % 2 == 0 else odd).add(q)
+    prev = now
+    rt = max(len(even), len(odd), 1)
+    cost[base] += rt
+    cnt[base] += 1
+    if "--print" in sys.argv:
+        print(f"{rt}  {x[:90]}")
+for k in cost:
+    print(f"{k:8s} n={cnt[k]:3d} rf={cost[k]:4d} avg={cost[k] / cnt[k]:.2f}")
+print("total", sum(cost.values()))
