@@ -334,6 +334,39 @@ __device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64
   }
 }
 
+// the lane holding candidate d after xsum<N> (inverse of xidx<N>)
+template <int N>
+__device__ __forceinline__ int xlane(int d) {
+  int lane = 0, c = N;
+#pragma unroll
+  for (int o = 16; o >= 1 && c > 1; o >>= 1) {
+    c >>= 1;
+    if (d & c) lane |= o;
+  }
+  return lane;
+}
+
+// per-row statistics, loaded one row ahead (after the row's key): the row window's mean, std and
+// flat flag, and for this lane's candidate b + xidx(lane) (clamped) the same three
+struct FinPre {
+  double mi, si, mc, sc;
+  bool fi, fc;
+};
+template <int SPAN>
+__device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64_t o, int64_t oo, int64_t i,
+                                          int64_t b, int lane) {
+  FinPre p;
+  p.mi = w.mu[o + i];
+  p.si = w.sig64[o + i];
+  p.fi = w.flat[o + i] != 0;
+  int64_t jc = b + xidx<SPAN>(lane);
+  jc = jc < 0 ? 0 : (jc >= wo.n_sub ? wo.n_sub - 1 : jc);
+  p.mc = wo.mu[oo + jc];
+  p.sc = wo.sig64[oo + jc];
+  p.fc = wo.flat[oo + jc] != 0;
+  return p;
+}
+
 template <typename T, int SPAN, int E>
 __global__ void __launch_bounds__(32 * kFinRegWarps)
 finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
@@ -357,32 +390,34 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
   const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
   auto row_of = [&](int rr) { const int64_t x = i_first + rr; return x < row_hi ? x : row_hi - 1; };
   auto base_of = [&](int64_t kw) { int64_t kb = 0; return key_arg(kw, words, &kb) ? kb : (int64_t)0; };
-  // prologue: row 0 staged, row 1's key in flight
+  // prologue: row 0 staged and its statistics requested, row 1's key in flight.  Every global
+  // load of a row is issued one row ahead (its key two rows ahead): no dependent load waits.
   int64_t kw_cur = key_word(keys, row_of(0), words);
   int64_t kw_nxt = key_word(keys, row_of(1), words);
   reg_stage<T, E, SPAN>(buf0, R, Ro, row_of(0), base_of(kw_cur), w.n, wo.n, lane);
   cp_async_commit();
+  FinPre pre = fin_pre<SPAN>(w, wo, o, oo, row_of(0), base_of(kw_cur), lane);
   for (int rr = 0; rr < kFinRows; ++rr) {
     const int64_t i_raw = i_first + rr;
     const bool live = i_raw < row_hi;
     const int64_t i = row_of(rr);
     const int64_t kw = kw_cur;
+    const FinPre cu = pre;
     T* cur = buf0 + (rr & 1) * B::SIZE;
-    // next row's windows into the other buffer (its key arrived during the previous row), and
-    // the key after it
-    if (rr + 1 < kFinRows)
-      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), base_of(kw_nxt), w.n, wo.n,
-                            lane);
+    if (rr + 1 < kFinRows) {
+      const int64_t bn = base_of(kw_nxt);
+      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), bn, w.n, wo.n, lane);
+      pre = fin_pre<SPAN>(w, wo, o, oo, row_of(rr + 1), bn, lane);
+    }
     cp_async_commit();
     kw_cur = kw_nxt;
     kw_nxt = key_word(keys, row_of(rr + 2 < kFinRows ? rr + 2 : kFinRows - 1), words);
     cp_async_wait1();
     __syncwarp();
-    const bool fi = w.flat[o + i] != 0;
     int64_t kb = 0;
     const bool has = key_arg(kw, words, &kb);
     const int64_t b = has ? kb : 0;
-    const double mi = w.mu[o + i];
+    const double mi = cu.mi;
     // ---- the SPAN candidate dot products, in registers --------------------------------------
     const T* xi = cur;
     const T* xo = cur + B::XI;
@@ -410,11 +445,11 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     double dd = inf;
     const int64_t jd = b + d;
     if (admissible(i, jd, wo.n_sub, excl)) {
-      if (wo.flat[oo + jd]) {
+      if (cu.fc) {
         dd = (double)m;
       } else {
-        const double cov = acc[0] - wo.mu[oo + jd] * asum;
-        dd = 2.0 * m - 2.0 * cov / (w.sig64[o + i] * wo.sig64[oo + jd]);
+        const double cov = acc[0] - cu.mc * asum;
+        dd = 2.0 * m - 2.0 * cov / (cu.si * cu.sc);
       }
     }
 #pragma unroll
@@ -427,14 +462,17 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
       }
     }
     const int64_t jr = dd < inf ? b + d : -1;
+    // the chosen member's statistics from the lane that prefetched them
+    const int src = xlane<SPAN>(jr >= 0 ? d : 0);
+    const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
+    const double sj = __shfl_sync(0xffffffffu, cu.sc, src);
+    const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
     // ---- the chosen member's distance by explicit differences (Def. 3) ----------------------
-    const bool exact = jr >= 0 && !wo.flat[oo + (jr >= 0 ? jr : 0)];
-    const int64_t je = exact ? jr : (b < 0 ? 0 : (b >= wo.n_sub ? wo.n_sub - 1 : b));
+    const bool exact = jr >= 0 && !fj;
     const int de = exact ? d : 0;
     double pe;
     {
-      const double mj = wo.mu[oo + je];
-      const double ii = 1.0 / w.sig64[o + i], ij = 1.0 / wo.sig64[oo + je];
+      const double ii = 1.0 / cu.si, ij = 1.0 / sj;
       double acc2 = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -450,7 +488,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     }
     double p;
     int64_t j;
-    if (fi) {
+    if (cu.fi) {
       const int64_t f = smallest_adm_flat(F, nf, i, excl);
       if (f >= 0) {
         p = 0.0;

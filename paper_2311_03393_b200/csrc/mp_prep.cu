@@ -46,40 +46,68 @@ template <> struct Q4<float> { using type = float4; };
 struct __align__(32) double4a { double x, y, z, w; };
 template <> struct Q4<double> { using type = double4a; };
 
+// sum of x[0..m) with four interleaved partial sums (fixed order: ((a0 + a1) + (a2 + a3)), so
+// each window's mean is the same number wherever it is computed); the chains are a quarter as
+// long as a sequential sum's
+__device__ __forceinline__ double window_sum(const double* x, int m) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int s = 0;
+  for (; s + 3 < m; s += 4) {
+    a0 += x[s];
+    a1 += x[s + 1];
+    a2 += x[s + 2];
+    a3 += x[s + 3];
+  }
+  for (; s < m; ++s) a0 += x[s];
+  return (a0 + a1) + (a2 + a3);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kPrepThreads)
 prep_kernel(MpDev w) {
-  extern __shared__ double xs[];  // R[i0-1 .. i0+kPrepThreads+m-1)
+  extern __shared__ double xs[];  // R[i0-1 .. i0+kPrepThreads+m-1), then the block's window means
   using QT = typename Q4<T>::type;
   const int g = blockIdx.y;
   const int64_t i0 = (int64_t)blockIdx.x * kPrepThreads;
   const int m = w.m;
   const T* r = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
   const int span = kPrepThreads + m;
+  double* smu = xs + span;  // smu[t] = mean of window i0 - 1 + t, t in [0, kPrepThreads]
   for (int s = threadIdx.x; s < span; s += kPrepThreads) {
     const int64_t t = i0 - 1 + s;
     xs[s] = (t >= 0 && t < w.n) ? (double)r[t] : 0.0;
   }
   __syncthreads();
+  // every window mean once per block (window i0 - 1 by thread 0 as well): thread i reads its
+  // predecessor's mean instead of summing that window again
+  smu[threadIdx.x + 1] = window_sum(xs + 1 + threadIdx.x, m) / m;
+  if (threadIdx.x == 0) smu[0] = window_sum(xs, m) / m;
+  __syncthreads();
   const int64_t i = i0 + threadIdx.x;
   if (i >= w.n_sub) return;
   const double* x = xs + 1 + threadIdx.x;  // x[s] = R[i+s]; x[-1] = R[i-1]
-  // mean of window i and of window i-1, same sequential order as each other's owner thread
-  double s1 = 0.0;
-  for (int s = 0; s < m; ++s) s1 += x[s];
-  const double mu = s1 / m;
-  double q = 0.0;
-  for (int s = 0; s < m; ++s) {
-    const double c = x[s] - mu;
-    q = __dadd_rn(q, __dmul_rn(c, c));  // no contraction: same rounding as the plain definition
+  const double mu = smu[threadIdx.x + 1];
+  double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+  {
+    int s = 0;
+    for (; s + 3 < m; s += 4) {  // no contraction: same rounding as the plain definition per term
+      const double c0 = x[s] - mu, c1 = x[s + 1] - mu, c2 = x[s + 2] - mu, c3 = x[s + 3] - mu;
+      q0 = __dadd_rn(q0, __dmul_rn(c0, c0));
+      q1 = __dadd_rn(q1, __dmul_rn(c1, c1));
+      q2 = __dadd_rn(q2, __dmul_rn(c2, c2));
+      q3 = __dadd_rn(q3, __dmul_rn(c3, c3));
+    }
+    for (; s < m; ++s) {
+      const double c = x[s] - mu;
+      q0 = __dadd_rn(q0, __dmul_rn(c, c));
+    }
   }
+  const double q = (q0 + q1) + (q2 + q3);
   const double sig = sqrt(q / m);
   const bool flat = !(sig > kFlatEps * (w.amax[g] + 1.0));
   double df = 0.0, dg = 0.0;
   if (i > 0) {
-    double s0 = 0.0;
-    for (int s = -1; s < m - 1; ++s) s0 += x[s];
-    const double mu_prev = s0 / m;
+    const double mu_prev = smu[threadIdx.x];
     df = (x[m - 1] - x[-1]) * 0.5;
     dg = (x[m - 1] - mu) + (x[-1] - mu_prev);
   }
@@ -165,7 +193,7 @@ cudaError_t launch_mp_prep(const MpDev& w, cudaStream_t st) {
     if (e) return e;
   }
   dim3 grid((unsigned)((w.n_sub + kPrepThreads - 1) / kPrepThreads), (unsigned)w.k);
-  const size_t smem = sizeof(double) * (kPrepThreads + w.m);
+  const size_t smem = sizeof(double) * (2 * kPrepThreads + w.m + 1);
   if (w.dtype == SKMP_F32) {
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(prep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
