@@ -731,7 +731,7 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   const size_t kq = (size_t)k * (size_t)w.ldq;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
-  const size_t oQ = take(qsz * kq), oMu = take(8 * kq), oSig = take(8 * kq), oFlat = take(kq),
+  const size_t oQ = take(qsz * kq), oMu = take(8 * kq), oSig = take(8 * kq), oISig = take(8 * kq), oFlat = take(kq),
                oAmax = take(8 * (size_t)k), oNf = take(4 * (size_t)k),
                oKeys = take(8 * (size_t)words * (size_t)k * (size_t)w.n_sub);
   cudaError_t e = dmalloc(&h->base, off, st);
@@ -743,6 +743,7 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   w.Q = b + oQ;
   w.mu = reinterpret_cast<double*>(b + oMu);
   w.sig64 = reinterpret_cast<double*>(b + oSig);
+  w.isig64 = reinterpret_cast<double*>(b + oISig);
   w.flat = reinterpret_cast<uint8_t*>(b + oFlat);
   w.amax = reinterpret_cast<double*>(b + oAmax);
   w.nflat = reinterpret_cast<int32_t*>(b + oNf);

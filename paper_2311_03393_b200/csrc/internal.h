@@ -126,6 +126,7 @@ struct MpDev {
   void* Q;                    // k x ldq x {df, dg, inv, 0} (dtype)
   double* mu;                 // k x ldq
   double* sig64;              // k x ldq  window population std (FP64)
+  double* isig64;             // k x ldq  1 / sig64 (FP64, one IEEE division; inf for sigma = 0)
   uint8_t* flat;              // k x ldq
   double* amax;               // k
   int32_t* nflat;             // k

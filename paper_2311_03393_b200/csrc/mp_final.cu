@@ -307,29 +307,39 @@ template <int E, int SPAN> struct RegBuf {
   static constexpr int SIZE = XI + XO;                 // elements per buffer
 };
 
-// stage row i's window and the candidate windows of base b (clamped reads: every staged value is
-// a finite series value; the ones past the windows are masked out of the sums)
+// stage row i's window and the candidate windows of base b: positions s < m of the row window
+// and t < m + SPAN - 1 of the candidates (the buffer tails stay zero from the kernel start, so
+// the masked products are 0 * 0).  Every copy of a lane is at a compile-time offset from one
+// global and one shared base (lane l's positions l + 32 q pad to l + l/E + q (32 + 32/E)); a
+// candidate window that leaves the series is staged with clamped reads (only inadmissible members
+// read clamped values; warp-uniform slow path at the two ends of the series).
 template <typename T, int E, int SPAN>
-__device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int64_t n,
+__device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int m,
                                           int64_t n_o, int lane) {
   using B = RegBuf<E, SPAN>;
-  T* xi = buf;
-  T* xo = buf + B::XI;
-  const int32_t ib = (int32_t)i, nn = (int32_t)n, ob = (int32_t)b, no = (int32_t)n_o;
+  T* xi = buf + pad_pos<E>(lane);
+  T* xo = buf + B::XI + pad_pos<E>(lane);
+  constexpr int QS = 32 + 32 / E;  // padded stride of q
+  const T* gi = R + i + lane;
 #pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int s = lane + 32 * q;
-    int32_t idx = ib + s;
-    idx = idx >= nn ? nn - 1 : idx;
-    cp_async_b(xi + pad_pos<E>(s), R + idx, (int)sizeof(T));
-  }
+  for (int q = 0; q < E; ++q)
+    if (lane + 32 * q < m) cp_async_b(xi + q * QS, gi + 32 * q, (int)sizeof(T));
+  const int no_used = m + SPAN - 1;
+  if (b >= 0 && b + no_used <= n_o) {
+    const T* go = Ro + b + lane;
 #pragma unroll
-  for (int q = 0; q < (B::NO + 31) / 32; ++q) {
-    const int t = lane + 32 * q;
-    if (t < B::NO) {
-      int32_t idx = ob + t;
-      idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);
-      cp_async_b(xo + pad_pos<E>(t), Ro + idx, (int)sizeof(T));
+    for (int q = 0; q < (B::NO + 31) / 32; ++q)
+      if (lane + 32 * q < no_used) cp_async_b(xo + q * QS, go + 32 * q, (int)sizeof(T));
+  } else {
+    const int32_t ob = (int32_t)b, no = (int32_t)n_o;
+#pragma unroll
+    for (int q = 0; q < (B::NO + 31) / 32; ++q) {
+      const int t = lane + 32 * q;
+      if (t < no_used) {
+        int32_t idx = ob + t;
+        idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);
+        cp_async_b(xo + q * QS, Ro + idx, (int)sizeof(T));
+      }
     }
   }
 }
@@ -346,10 +356,11 @@ __device__ __forceinline__ int xlane(int d) {
   return lane;
 }
 
-// per-row statistics, loaded one row ahead (after the row's key): the row window's mean, std and
-// flat flag, and for this lane's candidate b + xidx(lane) (clamped) the same three
+// per-row statistics, loaded one row ahead (after the row's key): the row window's mean,
+// inverse std and flat flag, and for this lane's candidate b + xidx(lane) (clamped) the same three
+// (inverse stds precomputed by mp_prep.cu: no FP64 division here)
 struct FinPre {
-  double mi, si, mc, sc;
+  double mi, ii, mc, ic;
   bool fi, fc;
 };
 template <int SPAN>
@@ -357,12 +368,12 @@ __device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64
                                           int64_t b, int lane) {
   FinPre p;
   p.mi = w.mu[o + i];
-  p.si = w.sig64[o + i];
+  p.ii = w.isig64[o + i];
   p.fi = w.flat[o + i] != 0;
   int64_t jc = b + xidx<SPAN>(lane);
   jc = jc < 0 ? 0 : (jc >= wo.n_sub ? wo.n_sub - 1 : jc);
   p.mc = wo.mu[oo + jc];
-  p.sc = wo.sig64[oo + jc];
+  p.ic = wo.isig64[oo + jc];
   p.fc = wo.flat[oo + jc] != 0;
   return p;
 }
@@ -394,7 +405,9 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
   // load of a row is issued one row ahead (its key two rows ahead): no dependent load waits.
   int64_t kw_cur = key_word(keys, row_of(0), words);
   int64_t kw_nxt = key_word(keys, row_of(1), words);
-  reg_stage<T, E, SPAN>(buf0, R, Ro, row_of(0), base_of(kw_cur), w.n, wo.n, lane);
+  for (int q = lane; q < 2 * B::SIZE; q += 32) buf0[q] = (T)0;  // tails stay zero (see reg_stage)
+  __syncwarp();
+  reg_stage<T, E, SPAN>(buf0, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, lane);
   cp_async_commit();
   FinPre pre = fin_pre<SPAN>(w, wo, o, oo, row_of(0), base_of(kw_cur), lane);
   for (int rr = 0; rr < kFinRows; ++rr) {
@@ -406,7 +419,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     T* cur = buf0 + (rr & 1) * B::SIZE;
     if (rr + 1 < kFinRows) {
       const int64_t bn = base_of(kw_nxt);
-      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), bn, w.n, wo.n, lane);
+      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), bn, m, wo.n, lane);
       pre = fin_pre<SPAN>(w, wo, o, oo, row_of(rr + 1), bn, lane);
     }
     cp_async_commit();
@@ -449,7 +462,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
         dd = (double)m;
       } else {
         const double cov = acc[0] - cu.mc * asum;
-        dd = 2.0 * m - 2.0 * cov / (cu.si * cu.sc);
+        dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
       }
     }
 #pragma unroll
@@ -465,14 +478,14 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     // the chosen member's statistics from the lane that prefetched them
     const int src = xlane<SPAN>(jr >= 0 ? d : 0);
     const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
-    const double sj = __shfl_sync(0xffffffffu, cu.sc, src);
+    const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
     const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
     // ---- the chosen member's distance by explicit differences (Def. 3) ----------------------
     const bool exact = jr >= 0 && !fj;
     const int de = exact ? d : 0;
     double pe;
     {
-      const double ii = 1.0 / cu.si, ij = 1.0 / sj;
+      const double ii = cu.ii;
       double acc2 = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {

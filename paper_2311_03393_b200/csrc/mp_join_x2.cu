@@ -121,6 +121,9 @@ struct Col {
 // in the odd register; SKMP_X2_BAL keeps the running column maxima as pairs {B, A}, i.e. group A's
 // maximum in an ODD register and B's in an even one, so every column update max3(CA, ka, la)
 // reads two of one parity and one of the other, and interleaves the row tree (tools/rf_model.py).
+#ifndef SKMP_X2_QT_LIVE
+#define SKMP_X2_QT_LIVE 0
+#endif
 #ifndef SKMP_X2_BAL
 #define SKMP_X2_BAL 1
 #endif
@@ -489,7 +492,9 @@ join_x2_kernel(JoinArgs a) {
   ColMax CM;
 #pragma unroll
   for (int d = 0; d < DG; ++d) CM.set(d, neg_inf<float>(), neg_inf<float>());
+#if SKMP_X2_QT_LIVE
   int qt = (int)(((i0 + dt) % RS) / DG);
+#endif
 
   for (int64_t r = i0; r < i1; r += C) {
     const int64_t rend = (r + C < i1) ? r + C : i1;
@@ -505,12 +510,22 @@ join_x2_kernel(JoinArgs a) {
     int64_t ib = r;
     const bool cmasked = diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub_c || rend > n_sub;
     for (int it = 0; it < nrot; ++it, ib += DG) {
+#if SKMP_X2_QT_LIVE
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
+#else
+      // ring row of this rotation's first column record, recomputed from the row index: keeping it
+      // live across the rotation cost a register the allocator spilled (one LDL per rotation,
+      // stalled on: 4 % of the join's stall samples, r1h ncu source page)
+      const int qt = (int)((((uint32_t)ib + (uint32_t)dt) / DG) % RSD);
+      const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
+#endif
       if (cmasked)
         rotation_x2<true>(cov, X, CM, &sm, rb, qt, qt1, ib, dt, lim, a, g);
       else
         rotation_x2<false>(cov, X, CM, &sm, rb, qt, qt1, ib, dt, lim, a, g);
+#if SKMP_X2_QT_LIVE
       qt = qt1;
+#endif
       rb = (rb + DG) & (2 * C - 1);
     }
     if (more) {

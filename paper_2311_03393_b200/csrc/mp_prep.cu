@@ -121,6 +121,7 @@ prep_kernel(MpDev w) {
   reinterpret_cast<QT*>(w.Q)[o] = qv;
   w.mu[o] = mu;
   w.sig64[o] = sig;
+  w.isig64[o] = 1.0 / sig;
   w.flat[o] = flat ? 1 : 0;
   // one atomic per warp: the lowest active lane adds the warp's flat count
   const unsigned act = __activemask();
