@@ -524,8 +524,9 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "join_traffic.json")))
-        if prof.get("config") == cfg.name:
-            traffic = prof["dram_bytes_per_launch"]
+        for ent in (prof if isinstance(prof, list) else [prof]):   # one entry per config (ncu captures)
+            if ent.get("config") == cfg.name and ent.get("world", 1) == world:
+                traffic = ent["dram_bytes_per_launch"]
     except Exception:
         pass
     sk_bytes = 2 * cfg.d * cfg.n * (4 if cfg.dtype == "f32" else 8) // world + \

@@ -22,7 +22,7 @@ for a, x in bl:
         if not m or o.startswith("RZ"):
             continue
         r = int(m.group(1)[1:])
-        wide = base in ("FFMA2", "FMUL2") and ".F32x2" in o
+        wide = (base in ("FFMA2", "FMUL2") and ".F32x2" in o) or base in ("DFMA", "DMUL", "DADD", "DSETP")
         if ".reuse" in o:
             now[slot] = r
         if prev.get(slot) == r:

@@ -75,7 +75,8 @@ def model(block):
             if not m or o.startswith("RZ"):
                 continue
             r = int(m.group(1)[1:])
-            wide = any(w in o for w in ("F32x2",)) or (base in ("FFMA2", "FMUL2", "FADD2") and ".F32" not in o)
+            wide = any(w in o for w in ("F32x2",)) or (base in ("FFMA2", "FMUL2", "FADD2") and ".F32" not in o) \
+                or base in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX")
             regs = [r, r + 1] if wide else [r]
             if ".reuse" in o:
                 reuse_now[slot] = r
@@ -86,7 +87,7 @@ def model(block):
         prev_reuse = reuse_now
         rt = max(len(even), len(odd), 1)
         rf += rt
-        if base in ("FFMA2", "FMUL2", "FADD2"):
+        if base in ("FFMA2", "FMUL2", "FADD2", "DFMA", "DMUL", "DADD", "DSETP"):
             fma += 2
         elif base in ("FFMA", "FMUL", "FADD", "IMAD"):
             fma += 1
