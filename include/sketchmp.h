@@ -178,8 +178,10 @@ typedef struct {
 typedef struct skmp_mp skmp_mp;  /* opaque join workspace: window statistics + profile keys */
 
 /* Window preparation (per-window mean/std in FP64 by direct sums, flat flags, recurrence terms)
- * and key initialisation.  R [dev] k x ld (dtype), n samples per series.  Synchronous (one D2H
- * of per-series flat counts).  Errors: INVALID_ARG, SERIES_TOO_SHORT, NO_ADMISSIBLE, CUDA, OOM.*/
+ * and key initialisation.  R [dev] k x ld (dtype), n samples per series.  Asynchronous: the
+ * per-series flat counts travel to the host behind the kernels and are waited for only when the
+ * host needs them (the inert flags of mp_finalize*).  R must stay valid until the join and the
+ * finalize have run.  Errors: INVALID_ARG, SERIES_TOO_SHORT, NO_ADMISSIBLE, CUDA, OOM.*/
 skmp_status mp_create(const void* R, int32_t k, int64_t n, int64_t ld, int32_t dtype,
                       const skmp_mp_cfg* cfg, void* stream, skmp_mp** out);
 
@@ -215,7 +217,8 @@ int32_t mp_tile_width(int32_t dtype);
 /* Finalize: keys -> P [dev] k x n_sub (dtype) and I [dev] k x n_sub (int64), inert [host] k.
  * Each entry's winning candidate set is resolved in FP64 (nearest admissible member, smallest
  * index on ties) and its distance recomputed from Def. 3 by explicit differences.
- * Requires the full diagonal range to have been joined.  Synchronous only for the inert copy.
+ * Requires the full diagonal range to have been joined.  Asynchronous when inert is NULL; with
+ * inert it waits for mp_create's flat counts (which normally arrived long before).
  * Errors: INVALID_ARG, CUDA. */
 skmp_status mp_finalize(skmp_mp* w, void* P, int64_t* I, uint8_t* inert, void* stream);
 /* Finalize only the windows [row_lo, row_hi) of every series (0 <= row_lo <= row_hi <= n_sub)

@@ -657,8 +657,14 @@ skmp_status skmp_trim(void) {
 struct skmp_mp {
   MpDev w;
   cudaStream_t st = nullptr;
+  // per-series flat counts reach the host asynchronously (pinned copy + event, issued by
+  // mp_create); host_flags() waits for them the first time the host needs them (finalize's
+  // inert flags, the streaming bookkeeping), so mp_create itself never blocks
   std::vector<int32_t> nflat;
   std::vector<uint8_t> inert;
+  int32_t* h_nflat = nullptr;  // pinned
+  cudaEvent_t flags_ev = nullptr;
+  bool flags_ready = false;
   void* base = nullptr;  // single allocation
 };
 
@@ -682,6 +688,17 @@ skmp_status mp_validate(const void* R, int32_t k, int64_t n, int64_t ld, int32_t
   }
   if (n_sub < 2 * (int64_t)(*excl) + 2)
     return set_error(SKMP_E_NO_ADMISSIBLE, "mp: n_sub < 2*excl + 2 (some row has no admissible neighbour)");
+  return SKMP_OK;
+}
+// wait (once) for mp_create's asynchronous copy of the per-series flat counts
+skmp_status host_flags(skmp_mp* h) {
+  if (h->flags_ready) return SKMP_OK;
+  SKMP_CUDA(cudaEventSynchronize(h->flags_ev));
+  const int k = h->w.k;
+  h->nflat.assign(h->h_nflat, h->h_nflat + k);
+  h->inert.assign((size_t)k, 0);
+  for (int g = 0; g < k; ++g) h->inert[(size_t)g] = h->nflat[(size_t)g] == h->w.n_sub;
+  h->flags_ready = true;
   return SKMP_OK;
 }
 }  // namespace
@@ -733,7 +750,8 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   const size_t oQ = take(qsz * kq), oMu = take(8 * kq), oSig = take(8 * kq), oISig = take(8 * kq), oFlat = take(kq),
                oAmax = take(8 * (size_t)k), oNf = take(4 * (size_t)k),
-               oKeys = take(8 * (size_t)words * (size_t)k * (size_t)w.n_sub);
+               oKeys = take(8 * (size_t)words * (size_t)k * (size_t)w.n_sub),
+               oFL = take(4 * (size_t)k * (size_t)w.n_sub);
   cudaError_t e = dmalloc(&h->base, off, st);
   if (e != cudaSuccess) {
     delete h;
@@ -748,31 +766,18 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   w.amax = reinterpret_cast<double*>(b + oAmax);
   w.nflat = reinterpret_cast<int32_t*>(b + oNf);
   w.keys = reinterpret_cast<int64_t*>(b + oKeys);
-  w.flat_list = nullptr;
+  w.flat_list = reinterpret_cast<int32_t*>(b + oFL);
   h->st = st;
   e = launch_mp_prep(w, st);
   if (e == cudaSuccess) e = launch_keys_init(w, st);
-  h->nflat.assign((size_t)k, 0);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(h->nflat.data(), w.nflat, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = launch_flat_lists(w, st);
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&h->h_nflat, sizeof(int32_t) * k);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->h_nflat, w.nflat, sizeof(int32_t) * k, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->flags_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(h->flags_ev, st);
   if (e != cudaSuccess) {
     mp_free(h);
     return cuda_error(e, "mp_create: window preparation");
-  }
-  h->inert.assign((size_t)k, 0);
-  bool any_flat = false;
-  for (int g = 0; g < k; ++g) {
-    h->inert[(size_t)g] = h->nflat[(size_t)g] == w.n_sub;
-    any_flat |= h->nflat[(size_t)g] > 0;
-  }
-  if (any_flat) {
-    e = dmalloc((void**)&w.flat_list, sizeof(int32_t) * (size_t)k * (size_t)w.n_sub, st);
-    if (e == cudaSuccess) e = launch_flat_lists(w, h->nflat.data(), st);
-    if (e != cudaSuccess) {
-      mp_free(h);
-      return cuda_error(e, "mp_create: flat lists");
-    }
   }
   *out = h;
   return ok();
@@ -892,7 +897,11 @@ skmp_status mp_finalize(skmp_mp* h, void* P, int64_t* I, uint8_t* inert, void* s
   if (h->w.excl < 0) return set_error(SKMP_E_INVALID_ARG, "mp_finalize: AB workspace; use mp_finalize_ab");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SKMP_CUDA(launch_mp_finalize(h->w, h->w, h->w.excl, P, I, st));
-  if (inert) memcpy(inert, h->inert.data(), h->inert.size());
+  if (inert) {
+    skmp_status s = host_flags(h);
+    if (s) return s;
+    memcpy(inert, h->inert.data(), h->inert.size());
+  }
   h->st = st;
   return ok();
 }
@@ -905,14 +914,22 @@ skmp_status mp_finalize_rows(skmp_mp* h, int64_t row_lo, int64_t row_hi, void* P
     return set_error(SKMP_E_INVALID_ARG, "mp_finalize_rows: need 0 <= row_lo <= row_hi <= n_sub");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SKMP_CUDA(launch_mp_finalize(h->w, h->w, h->w.excl, P, I, st, row_lo, row_hi));
-  if (inert) memcpy(inert, h->inert.data(), h->inert.size());
+  if (inert) {
+    skmp_status s = host_flags(h);
+    if (s) return s;
+    memcpy(inert, h->inert.data(), h->inert.size());
+  }
   h->st = st;
   return ok();
 }
 
 void mp_free(skmp_mp* h) {
   if (!h) return;
-  if (h->w.flat_list) cudaFreeAsync(h->w.flat_list, h->st);
+  if (h->flags_ev) {
+    cudaEventSynchronize(h->flags_ev);  // the pinned flag buffer may still be the copy's target
+    cudaEventDestroy(h->flags_ev);
+  }
+  if (h->h_nflat) cudaFreeHost(h->h_nflat);
   if (h->base) cudaFreeAsync(h->base, h->st);
   delete h;
 }
@@ -959,8 +976,12 @@ skmp_status mp_finalize_ab(skmp_mp* w, skmp_mp* other, int64_t row_lo, int64_t r
     return set_error(SKMP_E_INVALID_ARG, "mp_finalize_ab: need 0 <= row_lo <= row_hi <= n_sub");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   SKMP_CUDA(launch_mp_finalize(w->w, other->w, -1, P, I, st, row_lo, row_hi));
-  if (inert)  // reading 22: inert when both series of the group are entirely flat
+  if (inert) {  // reading 22: inert when both series of the group are entirely flat
+    skmp_status s = host_flags(w);
+    if (s == SKMP_OK) s = host_flags(other);
+    if (s) return s;
     for (int g = 0; g < w->w.k; ++g) inert[g] = w->inert[(size_t)g] && other->inert[(size_t)g];
+  }
   w->st = st;
   return ok();
 }
@@ -1050,7 +1071,10 @@ skmp_status mp_abjoin(const void* RA, int64_t nA, int64_t ldA, const void* RB, i
   if (s == SKMP_OK && inert) {
     // reading 6 for an AB-join: a group is inert when both its test and train sketch series
     // are entirely flat (an empty group)
-    for (int g = 0; g < k; ++g) inert[g] = a->inert[(size_t)g] && b->inert[(size_t)g];
+    s = host_flags(a);
+    if (s == SKMP_OK) s = host_flags(b);
+    if (s == SKMP_OK)
+      for (int g = 0; g < k; ++g) inert[g] = a->inert[(size_t)g] && b->inert[(size_t)g];
   }
   mp_free(a);
   mp_free(b);
@@ -1124,7 +1148,8 @@ skmp_status stream_create(const skmp_sketch* train, const skmp_mp_cfg* cfg, int6
     return cuda_error(e, "stream_create: allocate");
   }
   if ((s = mp_create_impl(h->Rtrain, train->k, train->n, train->n, train->dtype, cfg, stream, &h->train, true)) !=
-      SKMP_OK) {
+          SKMP_OK ||
+      (s = host_flags(h->train)) != SKMP_OK) {
     stream_free(h);
     return s;
   }
@@ -1220,6 +1245,11 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
       mp_free(a);
       return cuda_error(e, "stream_push: carried rows");
     }
+    if ((s = host_flags(a)) != SKMP_OK) {
+      h->state_valid = false;
+      mp_free(a);
+      return s;
+    }
     for (int g = 0; g < q.k; ++g) h->nflat[(size_t)g] += a->nflat[(size_t)g] - pred[(size_t)g];
     h->cur ^= 1;
     h->state_valid = true;
@@ -1252,6 +1282,7 @@ skmp_status stream_push(skmp_stream* h, const void* T, int64_t n_new, int64_t ld
                             cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) s = cuda_error(e, "stream_push: finalize");
   }
+  if (s == SKMP_OK) s = host_flags(a);
   if (s == SKMP_OK) {
     for (int g = 0; g < q.k; ++g) h->nflat[(size_t)g] += a->nflat[(size_t)g];
     h->n_test += n_new;

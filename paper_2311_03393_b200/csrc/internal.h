@@ -131,7 +131,7 @@ struct MpDev {
   double* amax;               // k
   int32_t* nflat;             // k
   int64_t* keys;              // k x n_sub x words
-  int32_t* flat_list;         // k x n_sub (only filled for series with nflat > 0)
+  int32_t* flat_list;         // k x n_sub (filled only for series with nflat > 0)
 };
 // series per join chunk: as many as keep the chunk's operand records, window means and keys
 // (row and column side) within ~48 MB of the 126 MB L2
@@ -156,7 +156,9 @@ cudaError_t launch_mp_join(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t
 cudaError_t launch_mp_join_x2(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi,
                               const int64_t* d_tile_prefix, int64_t nblk, int64_t ntiles, int64_t blk0,
                               cudaStream_t st);
-cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st);
+// per-series sorted flat-window lists (w.flat_list, k x n_sub) for the series whose device count
+// w.nflat is non-zero (the others' kernels exit at once)
+cudaError_t launch_flat_lists(const MpDev& w, cudaStream_t st);
 // rows of w resolved against neighbours in wo (self-join: wo = w, excl >= 0; AB-join: excl = -1)
 // (rows [row_lo, row_hi) only; row_hi < 0 -> all rows)
 cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* P, int64_t* I,

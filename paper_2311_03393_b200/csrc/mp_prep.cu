@@ -142,13 +142,14 @@ __global__ void keys_init_kernel(int64_t* keys, int64_t count, int words) {
   }
 }
 
-// Ordered compaction of the flat-window indices of one series (single CTA; launched only for
-// series that have flat windows, which is rare).
+// Ordered compaction of the flat-window indices of one series per CTA; series without flat
+// windows (the device count, computed by prep_kernel) return at once.
 __global__ void flat_list_kernel(const uint8_t* __restrict__ flat, int64_t ldq, int64_t n_sub,
-                                 int32_t* __restrict__ list, const int32_t* __restrict__ series) {
+                                 int32_t* __restrict__ list, const int32_t* __restrict__ nflat) {
   __shared__ int32_t wsum[32];
   __shared__ int32_t base_sh;
-  const int g = series[blockIdx.x];
+  const int g = blockIdx.x;
+  if (nflat[g] == 0) return;
   const uint8_t* f = flat + (int64_t)g * ldq;
   int32_t* out = list + (int64_t)g * n_sub;
   if (threadIdx.x == 0) base_sh = 0;
@@ -220,30 +221,10 @@ cudaError_t launch_keys_init(const MpDev& w, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_flat_lists(const MpDev& w, const int32_t* h_nflat, cudaStream_t st) {
-  // simple and robust: one small device array of series ids
-  int nser = 0;
-  for (int g = 0; g < w.k; ++g) nser += h_nflat[g] > 0;
-  if (nser == 0) return cudaSuccess;
-  int32_t* d_ids = nullptr;
-  cudaError_t e = dmalloc((void**)&d_ids, sizeof(int32_t) * nser, st);
-  if (e) return e;
-  int32_t* h_ids = nullptr;
-  e = cudaMallocHost(&h_ids, sizeof(int32_t) * nser);
-  if (e) return e;
-  int q = 0;
-  for (int g = 0; g < w.k; ++g)
-    if (h_nflat[g] > 0) h_ids[q++] = g;
-  e = cudaMemcpyAsync(d_ids, h_ids, sizeof(int32_t) * nser, cudaMemcpyHostToDevice, st);
-  if (e) return e;
-  flat_list_kernel<<<nser, 1024, 0, st>>>(w.flat, w.ldq, w.n_sub, w.flat_list, d_ids);
+cudaError_t launch_flat_lists(const MpDev& w, cudaStream_t st) {
+  flat_list_kernel<<<w.k, 1024, 0, st>>>(w.flat, w.ldq, w.n_sub, w.flat_list, w.nflat);
   count_launches(1);
-  e = cudaGetLastError();
-  if (e) return e;
-  e = cudaStreamSynchronize(st);  // h_ids must outlive the copy
-  cudaFreeHost(h_ids);
-  if (e) return e;
-  return cudaFreeAsync(d_ids, st);
+  return cudaGetLastError();
 }
 
 }  // namespace skmp
