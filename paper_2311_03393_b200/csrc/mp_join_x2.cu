@@ -121,8 +121,12 @@ struct Col {
 // in the odd register; SKMP_X2_BAL keeps the running column maxima as pairs {B, A}, i.e. group A's
 // maximum in an ODD register and B's in an even one, so every column update max3(CA, ka, la)
 // reads two of one parity and one of the other, and interleaves the row tree (tools/rf_model.py).
-#ifndef SKMP_X2_QT_LIVE
-#define SKMP_X2_QT_LIVE 0
+// How a rotation finds the ring row of its first column record (SKMP_X2_QT): 0 = a live counter
+// (the allocator spills it: one LDL per rotation), 1 = recomputed from the row index ((ib+dt)/DG
+// mod RSD: an IMAD.HI + IMAD on the saturated FMA pipe), 2 = a rotation counter U (wraps at RSD,
+// the same for the whole warp) plus the lane: ALU-only, 3 = kept in shared memory per thread
+#ifndef SKMP_X2_QT
+#define SKMP_X2_QT 2
 #endif
 #ifndef SKMP_X2_BAL
 #define SKMP_X2_BAL 1
@@ -492,8 +496,13 @@ join_x2_kernel(JoinArgs a) {
   ColMax CM;
 #pragma unroll
   for (int d = 0; d < DG; ++d) CM.set(d, neg_inf<float>(), neg_inf<float>());
-#if SKMP_X2_QT_LIVE
+#if SKMP_X2_QT == 0
   int qt = (int)(((i0 + dt) % RS) / DG);
+#elif SKMP_X2_QT == 2
+  int qU = (int)(((i0 + delta0) / DG) % RSD);  // ((ib + delta0) / DG) mod RSD of the current rotation
+#elif SKMP_X2_QT == 3
+  __shared__ int s_qt[NT];
+  s_qt[tid] = (int)(((i0 + dt) % RS) / DG);
 #endif
 
   for (int64_t r = i0; r < i1; r += C) {
@@ -510,20 +519,26 @@ join_x2_kernel(JoinArgs a) {
     int64_t ib = r;
     const bool cmasked = diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub_c || rend > n_sub;
     for (int it = 0; it < nrot; ++it, ib += DG) {
-#if SKMP_X2_QT_LIVE
+#if SKMP_X2_QT == 0
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
-#else
-      // ring row of this rotation's first column record, recomputed from the row index: keeping it
-      // live across the rotation cost a register the allocator spilled (one LDL per rotation,
-      // stalled on: 4 % of the join's stall samples, r1h ncu source page)
+#elif SKMP_X2_QT == 1
       const int qt = (int)((((uint32_t)ib + (uint32_t)dt) / DG) % RSD);
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
+#elif SKMP_X2_QT == 2
+      int qt = qU + tid;  // tid < NT <= RSD: one conditional subtraction
+      qt = qt >= RSD ? qt - RSD : qt;
+      const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
+      qU = (qU + 1 == RSD) ? 0 : qU + 1;
+#else
+      const int qt = s_qt[tid];
+      const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
+      s_qt[tid] = qt1;
 #endif
       if (cmasked)
         rotation_x2<true>(cov, X, CM, &sm, rb, qt, qt1, ib, dt, lim, a, g);
       else
         rotation_x2<false>(cov, X, CM, &sm, rb, qt, qt1, ib, dt, lim, a, g);
-#if SKMP_X2_QT_LIVE
+#if SKMP_X2_QT == 0
       qt = qt1;
 #endif
       rb = (rb + DG) & (2 * C - 1);
