@@ -297,7 +297,12 @@ __device__ __forceinline__ void cp_async_b(void* smem, const void* gmem, int byt
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-constexpr int kFinRegWarps = 4;  // warps per CTA (~90 registers: 5 CTAs = 20 warps per SM)
+constexpr int kFinRegWarps = 4;
+// squared distances below this are recomputed by explicit differences (the dot-product form
+// 2m - 2 cov / (sigma_i sigma_j) loses ~1e-14 absolute to cancellation: at dd >= 1 that is
+// < 1e-13 relative in P, far inside the 1e-9 FP64 bar; near-duplicate windows need the
+// explicit form)
+constexpr double kFinExplicitBelow = 1.0;  // warps per CTA (~90 registers: 5 CTAs = 20 warps per SM)
 template <int E> __host__ __device__ constexpr int pad_pos(int s) { return s + s / E; }
 template <int E, int SPAN> struct RegBuf {
   static constexpr int NI = 32 * E;                    // row window positions (>= m)
@@ -313,7 +318,7 @@ template <int E, int SPAN> struct RegBuf {
 // global and one shared base (lane l's positions l + 32 q pad to l + l/E + q (32 + 32/E)); a
 // candidate window that leaves the series is staged with clamped reads (only inadmissible members
 // read clamped values; warp-uniform slow path at the two ends of the series).
-template <typename T, int E, int SPAN>
+template <typename T, int E, int SPAN, bool FULL>
 __device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int m,
                                           int64_t n_o, int lane) {
   using B = RegBuf<E, SPAN>;
@@ -323,7 +328,7 @@ __device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64
   const T* gi = R + i + lane;
 #pragma unroll
   for (int q = 0; q < E; ++q)
-    if (lane + 32 * q < m) cp_async_b(xi + q * QS, gi + 32 * q, (int)sizeof(T));
+    if (FULL || lane + 32 * q < m) cp_async_b(xi + q * QS, gi + 32 * q, (int)sizeof(T));
   const int no_used = m + SPAN - 1;
   if (b >= 0 && b + no_used <= n_o) {
     const T* go = Ro + b + lane;
@@ -378,7 +383,7 @@ __device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64
   return p;
 }
 
-template <typename T, int SPAN, int E>
+template <typename T, int SPAN, int E, bool FULL>
 __global__ void __launch_bounds__(32 * kFinRegWarps)
 finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
                     int64_t* __restrict__ I) {
@@ -407,7 +412,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
   int64_t kw_nxt = key_word(keys, row_of(1), words);
   for (int q = lane; q < 2 * B::SIZE; q += 32) buf0[q] = (T)0;  // tails stay zero (see reg_stage)
   __syncwarp();
-  reg_stage<T, E, SPAN>(buf0, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, lane);
+  reg_stage<T, E, SPAN, FULL>(buf0, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, lane);
   cp_async_commit();
   FinPre pre = fin_pre<SPAN>(w, wo, o, oo, row_of(0), base_of(kw_cur), lane);
   for (int rr = 0; rr < kFinRows; ++rr) {
@@ -419,7 +424,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     T* cur = buf0 + (rr & 1) * B::SIZE;
     if (rr + 1 < kFinRows) {
       const int64_t bn = base_of(kw_nxt);
-      reg_stage<T, E, SPAN>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), bn, m, wo.n, lane);
+      reg_stage<T, E, SPAN, FULL>(buf0 + ((rr + 1) & 1) * B::SIZE, R, Ro, row_of(rr + 1), bn, m, wo.n, lane);
       pre = fin_pre<SPAN>(w, wo, o, oo, row_of(rr + 1), bn, lane);
     }
     cp_async_commit();
@@ -438,7 +443,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int s = E * lane + e;
-      a[e] = s < m ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
+      a[e] = (FULL || s < m) ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
     }
 #pragma unroll
     for (int t = 0; t < E + SPAN - 1; ++t) wv[t] = (double)xo[pad_pos<E>(E * lane + t)];
@@ -465,8 +470,10 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
         dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
       }
     }
+    // argmin over the SPAN candidates: the 32 / SPAN lanes of a candidate hold the same value
+    // (xidx ignores the low lane bits), so only the high log2(SPAN) butterfly rounds are needed
 #pragma unroll
-    for (int q = 16; q >= 1; q >>= 1) {
+    for (int q = 16; q >= 32 / SPAN; q >>= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, dd, q);
       const int oi = __shfl_xor_sync(0xffffffffu, d, q);
       if (od < dd || (od == dd && oi < d)) {
@@ -480,11 +487,13 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
     const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
     const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
-    // ---- the chosen member's distance by explicit differences (Def. 3) ----------------------
+    // ---- the chosen member's distance: sqrt(dd) from the centred FP64 dot product, and for a
+    // near neighbour (dd < 1, where the cancellation in 2m - 2 cov / (sigma sigma) would show)
+    // recomputed by explicit differences (Def. 3); warp-uniform branch ------------------------
     const bool exact = jr >= 0 && !fj;
     const int de = exact ? d : 0;
-    double pe;
-    {
+    double pe = sqrt(dd > 0.0 ? dd : 0.0);
+    if (exact && dd < kFinExplicitBelow) {
       const double ii = cu.ii;
       double acc2 = 0.0;
 #pragma unroll
@@ -493,7 +502,7 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
         const double zi = __dmul_rn(a[e], ii);
         const double zj = __dmul_rn((double)xo[pad_pos<E>(s + de)] - mj, ij);
         const double df = zi - zj;
-        acc2 = s < m ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
+        acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
       }
 #pragma unroll
       for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
@@ -551,16 +560,18 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
   const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
 #define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
-#define SKMP_FINR(TT, SP, EE) \
-  finalize_reg_kernel<TT, SP, EE><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
   const int E = w.m <= 64 ? 2 : (w.m <= 128 ? 4 : (w.m <= 256 ? 8 : 0));
   if (E > 0 && (w.span == 4 || w.span == 8) && fin_reg_enabled()) {
     const int64_t perr = (int64_t)kFinRegWarps * kFinRows;
     grid.x = (unsigned)((row_hi - row_lo + perr - 1) / perr);
     const int ntr = 32 * kFinRegWarps;
-#undef SKMP_FINR
-#define SKMP_FINR(TT, SP, EE) \
-  finalize_reg_kernel<TT, SP, EE><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
+#define SKMP_FINR(TT, SP, EE)                                                                                    \
+  do {                                                                                                          \
+    if (w.m == 32 * (EE))                                                                                       \
+      finalize_reg_kernel<TT, SP, EE, true><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+    else                                                                                                        \
+      finalize_reg_kernel<TT, SP, EE, false><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+  } while (0)
     if (w.span == 8) {
       if (E == 2) { if (f32) SKMP_FINR(float, 8, 2); else SKMP_FINR(double, 8, 2); }
       else if (E == 4) { if (f32) SKMP_FINR(float, 8, 4); else SKMP_FINR(double, 8, 4); }

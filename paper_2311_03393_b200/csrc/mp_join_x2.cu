@@ -126,7 +126,7 @@ struct Col {
 // mod RSD: an IMAD.HI + IMAD on the saturated FMA pipe), 2 = a rotation counter U (wraps at RSD,
 // the same for the whole warp) plus the lane: ALU-only, 3 = kept in shared memory per thread
 #ifndef SKMP_X2_QT
-#define SKMP_X2_QT 2
+#define SKMP_X2_QT 3
 #endif
 #ifndef SKMP_X2_BAL
 #define SKMP_X2_BAL 1

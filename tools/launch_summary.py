@@ -1,12 +1,16 @@
 """Summarise an ncu launch-list CSV (gpu__time_duration.sum, optionally dram bytes) as a markdown
 table of per-kernel launches, time and share of the profiled steps.
-usage: python tools/launch_summary.py <launches.csv> [title]"""
+usage: python tools/launch_summary.py <launches.csv> [title] [--ours]
+--ours: only libsketchmp.so's kernels (drops torch's input-generation kernels, which run before
+the timed region)."""
 import collections
 import csv
 import sys
 
 path = sys.argv[1]
-title = sys.argv[2] if len(sys.argv) > 2 else path
+args = [a for a in sys.argv[2:] if not a.startswith("--")]
+title = args[0] if args else path
+ours = "--ours" in sys.argv
 rows = list(csv.reader(open(path)))
 start = next(k for k, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[start]
@@ -20,6 +24,8 @@ for r in rows[start + 1:]:
     try:
         v = float(r[iV].replace(",", ""))
     except ValueError:
+        continue
+    if ours and (r[iN].startswith("void at::") or r[iN].startswith("at::") or "at::native" in r[iN]):
         continue
     name = r[iN].split("(")[0]
     name = name.replace("void ", "").replace("skmp::", "").replace("<unnamed>::", "").replace("unnamed>::", "").split("<")[0]
