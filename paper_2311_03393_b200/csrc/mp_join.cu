@@ -41,6 +41,21 @@ namespace {
 using namespace join;
 
 
+// FP64 variant (SKMP_F64_HI): the cell values are rho' = rho + 2 in [1, 3] (the +2 rides in the last
+// FMA), positive doubles whose high 32-bit words order like the doubles.  Row maxima are reduced
+// on those high words (integer max on one register per cell instead of DSETP + two FSEL on a
+// register pair: 2 vs 6 register-file cycles per merged value, B300_MICROARCH.md RF banking) and
+// serve only as a FILTER: x >= y implies hi(x) >= hi(y), so no row that beats its threshold is
+// missed; a passing row's exact FP64 maximum is formed on the rare publish path.  Column maxima
+// stay exact FP64.  Thresholds in shared memory hold rho'; keys hold rho' - 2 (exact: Sterbenz),
+// i.e. rho rounded once more at 2^-51 absolute (documented ties at that level only).
+#ifndef SKMP_F64_HI
+#define SKMP_F64_HI 1
+#endif
+template <typename T> __device__ __forceinline__ T rho_shift() { return (T)0; }
+template <> __device__ __forceinline__ double rho_shift<double>() { return SKMP_F64_HI ? 2.0 : 0.0; }
+__device__ __forceinline__ int hi_word(double x) { return __double2hiint(x); }
+
 // Rare path: a row / column candidate beat its shared-memory threshold.  Out of line so that
 // none of its address arithmetic is hoisted into the hot loop.  The published argument is the
 // smallest index of the candidate's D-cell set (see mp_final.cu): row i's cells in this thread
@@ -49,20 +64,21 @@ template <typename T, int D>
 SKMP_PUB_ATTR void publish_pair(int64_t* keys, int64_t* keysc, typename JT<T>::Q* rowq, T* cthr, int rb_u,
                                           int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
                                           T colv0, T colv1) {
+  const T sh = rho_shift<T>();
   if (rowa >= rowq[rb_u].w) {
-    publish(keys, i_u, rowa, i_u + dt);
+    publish(keys, i_u, rowa - sh, i_u + dt);
     rowq[rb_u].w = rowa;
   }
   if (rowb >= rowq[rb_u + 1].w) {
-    publish(keys, i_u + 1, rowb, i_u + 1 + dt);
+    publish(keys, i_u + 1, rowb - sh, i_u + 1 + dt);
     rowq[rb_u + 1].w = rowb;
   }
   if (colv0 >= cthr[ct0]) {
-    publish(keysc, i_u + dt, colv0, i_u - (D - 1));
+    publish(keysc, i_u + dt, colv0 - sh, i_u - (D - 1));
     cthr[ct0] = colv0;
   }
   if (colv1 >= cthr[ct1]) {
-    publish(keysc, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
+    publish(keysc, i_u + 1 + dt, colv1 - sh, i_u + 1 - (D - 1));
     cthr[ct1] = colv1;
   }
 }
@@ -114,7 +130,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
       const Q& x = X[(u + d) % D];
       cov[d] = fma(ra.x, x.y, cov[d]);
       cov[d] = fma(x.x, ra.y, cov[d]);
-      ka[d] = (cov[d] * x.z) * ra.z;  // rho(i, j) = cov inv_j inv_i
+      ka[d] = fma(cov[d] * x.z, ra.z, rho_shift<T>());  // rho(i, j) = cov inv_j inv_i (+ shift)
     }
     if (MASKED) {
 #pragma unroll
@@ -130,7 +146,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
       const Q& x = X[(u + 1 + d) % D];
       cov[d] = fma(rbq.x, x.y, cov[d]);
       cov[d] = fma(x.x, rbq.y, cov[d]);
-      kb[d] = (cov[d] * x.z) * rbq.z;
+      kb[d] = fma(cov[d] * x.z, rbq.z, rho_shift<T>());
     }
     if (MASKED) {
 #pragma unroll
@@ -142,18 +158,35 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = max3(CK[(u + d) % D], ka[d], kb[d - 1]);
     CK[(u + D - 1) % D] = max2(ka[D - 1], kb[D - 2]);  // column entered at row u
     CK[u % D] = kb[D - 1];                              // column entered at row u+1
-    // -- row maxima over the D slots --
-    const T rowa = tree_max<T, D>(ka);
-    const T rowb = tree_max<T, D>(kb);
     // -- check-then-publish (rare) --
     // row thresholds ride in the row records' 4th word (ra.w, rbq.w): no extra loads
     // ">=": a candidate EQUAL to the current best is published too, so exact ties always reach
     // the atomic (smallest set wins) and keys do not depend on the tile order / band split
-    const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
-                     (colv1 >= cth0[((u + 1) % D) * RSD]);
-    if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
-      publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
-                         ib + u, dt, rowa, rowb, colv0, colv1);
+    if constexpr (sizeof(T) == 8 && SKMP_F64_HI) {
+      // row maxima on the high words as a filter, the exact maxima only on the rare path
+      int ha = hi_word(ka[0]), hb = hi_word(kb[0]);
+#pragma unroll
+      for (int d = 1; d < D; ++d) {
+        ha = max(ha, hi_word(ka[d]));
+        hb = max(hb, hi_word(kb[d]));
+      }
+      const bool hit = (ha >= hi_word(ra.w)) | (hb >= hi_word(rbq.w)) | (colv0 >= cth0[(u % D) * RSD]) |
+                       (colv1 >= cth0[((u + 1) % D) * RSD]);
+      if (__any_sync(0xffffffffu, hit)) {
+        const T rowa = tree_max<T, D>(ka);
+        const T rowb = tree_max<T, D>(kb);
+        publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+                           ib + u, dt, rowa, rowb, colv0, colv1);
+      }
+    } else {
+      const T rowa = tree_max<T, D>(ka);
+      const T rowb = tree_max<T, D>(kb);
+      const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
+                       (colv1 >= cth0[((u + 1) % D) * RSD]);
+      if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
+        publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+                           ib + u, dt, rowa, rowb, colv0, colv1);
+      }
     }
   }
 }
@@ -231,7 +264,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int e = tid; e < W + C; e += NT) {
     const int64_t c = i0 + delta0 + e;
     stage_q<T>(&ring[G::pos(c)], &qc[c]);
-    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
+    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
   }
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
@@ -241,7 +274,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // row thresholds go into the staged row records' 4th word once the copies have landed
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
-    rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
+    rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
   }
   __syncthreads();  // (one warp per CTA: a warp barrier; kept generic for NT > 32)
 
@@ -269,10 +302,10 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
       for (int e = 0; e < CPT; ++e) {
         const int64_t nc = r + delta0 + W + C + tid + e * NT;
         stage_q<T>(&ring[G::pos(nc)], &qc[nc]);
-        nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) : pos_inf<T>();
+        nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
         const int64_t nr = r + C + tid + e * NT;
         stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
-        nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) : pos_inf<T>();
+        nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
       }
     }
 
@@ -315,7 +348,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int x = 0; x < D - 1; ++x) {
     const T v = CK[x];
     const int64_t c = i1 + dt + x;
-    if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v, c - dt - (D - 1));
+    if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v - rho_shift<T>(), c - dt - (D - 1));
   }
 }
 
