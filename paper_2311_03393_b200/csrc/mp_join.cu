@@ -325,6 +325,8 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     const int64_t jb = i0 + dt;
 #pragma unroll
     for (int d = 0; d < D - 1; ++d) w[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
+    // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i)
+    double asum = 0.0;
     for (int s0 = 0; s0 < a.m; s0 += D) {
 #pragma unroll
       for (int e = 0; e < D; ++e) {
@@ -333,11 +335,14 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
           const int64_t t = jb + s + D - 1;
           w[(e + D - 1) % D] = (t < a.nc) ? (double)Rc[t] : 0.0;
           const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
+          asum += av;
 #pragma unroll
-          for (int d = 0; d < D; ++d) acc[d] = fma(av, w[(e + d) % D] - mub[d], acc[d]);
+          for (int d = 0; d < D; ++d) acc[d] = fma(av, w[(e + d) % D], acc[d]);
         }
       }
     }
+#pragma unroll
+    for (int d = 0; d < D; ++d) acc[d] = fma(-mub[d], asum, acc[d]);
     const Q qi = q[i0];
 #pragma unroll
     for (int d = 0; d < D; ++d) {

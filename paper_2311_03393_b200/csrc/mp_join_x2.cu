@@ -448,6 +448,9 @@ join_x2_kernel(JoinArgs a) {
       wa[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
       wb[d] = (jb + H + d < a.nc) ? (double)Rc[jb + H + d] : 0.0;
     }
+    // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i): one FP64 FMA
+    // per term instead of a subtraction and an FMA (the seeds are rounded to FP32 afterwards)
+    double asum = 0.0;
     for (int s0 = 0; s0 < a.m; s0 += DG) {
 #pragma unroll
       for (int u = 0; u < DG; ++u) {
@@ -457,14 +460,17 @@ join_x2_kernel(JoinArgs a) {
           wa[(u + DG - 1) % DG] = (t < a.nc) ? (double)Rc[t] : 0.0;
           wb[(u + DG - 1) % DG] = (t + H < a.nc) ? (double)Rc[t + H] : 0.0;
           const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
+          asum += av;
 #pragma unroll
           for (int d = 0; d < DG; ++d) {
-            acc[d] = fma(av, wa[(u + d) % DG] - mub[d], acc[d]);
-            acc[DG + d] = fma(av, wb[(u + d) % DG] - mub[DG + d], acc[DG + d]);
+            acc[d] = fma(av, wa[(u + d) % DG], acc[d]);
+            acc[DG + d] = fma(av, wb[(u + d) % DG], acc[DG + d]);
           }
         }
       }
     }
+#pragma unroll
+    for (int e = 0; e < 2 * DG; ++e) acc[e] = fma(-mub[e], asum, acc[e]);
     const float4 qi = q[i0];
     float c32[2 * DG];
 #pragma unroll
