@@ -30,7 +30,6 @@
 //    tiles start at multiples of L, diagonal blocks at multiples of W), so per-cell arithmetic
 //    is independent of how diagonals are split into bands/GPUs -> bit-identical keys.
 #include <cuda_runtime.h>
-#include <limits.h>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -42,21 +41,6 @@ namespace {
 using namespace join;
 
 
-// FP64 variant (SKMP_F64_HI): the cell values are rho' = rho + 2 in [1, 3] (the +2 rides in the last
-// FMA), positive doubles whose high 32-bit words order like the doubles.  Row maxima are reduced
-// on those high words (integer max on one register per cell instead of DSETP + two FSEL on a
-// register pair: 2 vs 6 register-file cycles per merged value, B300_MICROARCH.md RF banking) and
-// serve only as a FILTER: x >= y implies hi(x) >= hi(y), so no row that beats its threshold is
-// missed; a passing row's exact FP64 maximum is formed on the rare publish path.  Column maxima
-// stay exact FP64.  Thresholds in shared memory hold rho'; keys hold rho' - 2 (exact: Sterbenz),
-// i.e. rho rounded once more at 2^-51 absolute (documented ties at that level only).
-#ifndef SKMP_F64_HI
-#define SKMP_F64_HI 1
-#endif
-template <typename T> __device__ __forceinline__ T rho_shift() { return (T)0; }
-template <> __device__ __forceinline__ double rho_shift<double>() { return SKMP_F64_HI ? 2.0 : 0.0; }
-__device__ __forceinline__ int hi_word(double x) { return __double2hiint(x); }
-
 // Rare path: a row / column candidate beat its shared-memory threshold.  Out of line so that
 // none of its address arithmetic is hoisted into the hot loop.  The published argument is the
 // smallest index of the candidate's D-cell set (see mp_final.cu): row i's cells in this thread
@@ -65,21 +49,20 @@ template <typename T, int D>
 SKMP_PUB_ATTR void publish_pair(int64_t* keys, int64_t* keysc, typename JT<T>::Q* rowq, T* cthr, int rb_u,
                                           int ct0, int ct1, int64_t i_u, int64_t dt, T rowa, T rowb,
                                           T colv0, T colv1) {
-  const T sh = rho_shift<T>();
   if (rowa >= rowq[rb_u].w) {
-    publish(keys, i_u, rowa - sh, i_u + dt);
+    publish(keys, i_u, rowa, i_u + dt);
     rowq[rb_u].w = rowa;
   }
   if (rowb >= rowq[rb_u + 1].w) {
-    publish(keys, i_u + 1, rowb - sh, i_u + 1 + dt);
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt);
     rowq[rb_u + 1].w = rowb;
   }
   if (colv0 >= cthr[ct0]) {
-    publish(keysc, i_u + dt, colv0 - sh, i_u - (D - 1));
+    publish(keysc, i_u + dt, colv0, i_u - (D - 1));
     cthr[ct0] = colv0;
   }
   if (colv1 >= cthr[ct1]) {
-    publish(keysc, i_u + 1 + dt, colv1 - sh, i_u + 1 - (D - 1));
+    publish(keysc, i_u + 1 + dt, colv1, i_u + 1 - (D - 1));
     cthr[ct1] = colv1;
   }
 }
@@ -109,68 +92,16 @@ __device__ __forceinline__ void stage_q(typename JT<T>::Q* dst, const typename J
     cp_async16(reinterpret_cast<char*>(dst) + 16 * q, reinterpret_cast<const char*>(src) + 16 * q);
 }
 
-// SKMP_F64_COLHI: the FP64 column maxima are reduced on the high words too (a filter like the
-// rows'); a column that passes it gets its exact FP64 maximum by stepping each of its cells'
-// covariances back along their diagonals from the current row (the row / column records of
-// the last D rows are still staged; the next chunk's prefetch is issued after the chunk's first
-// rotation for that reason).  The stepped-back covariance is the forward one up to FP64
-// rounding (deterministic per tile, so keys stay band-split invariant); the finalize resolves
-// the winning set exactly either way.
-#ifndef SKMP_F64_COLHI
-#define SKMP_F64_COLHI 1
-#endif
-
-// exact rho' over the cells of column c held by this thread, rows [max(lo, c-dt-D+1), min(ir, c-dt)]
-// (slot d = c - row - dt), from the covariances at row ir; -inf if none is valid
-template <int D> struct ColState {  // passed by value: no local-memory copy of the registers
-  double cov[D];
-  int lim[D];
-};
-template <int D, int RSD, int C2>
-__device__ __noinline__ double col_exact(ColState<D> st, int64_t c, int64_t ir, int64_t lo, int64_t dt,
-                                         const dq4* rowq, const dq4* ring) {
-  constexpr int RS = RSD * D;
-  double best = neg_inf<double>();
-  const dq4& xc = ring[(int)((c % RS) % D) * RSD + (int)((c % RS) / D)];
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    const int64_t it = c - dt - d;
-    if (it < lo || it > ir || it >= st.lim[d]) continue;
-    double x = st.cov[d];
-    for (int64_t rr = ir; rr > it; --rr) {  // back along diagonal dt + d
-      const dq4& rq = rowq[(int)(rr & (C2 - 1))];
-      const int64_t col = rr + dt + d;
-      const dq4& cq = ring[(int)((col % RS) % D) * RSD + (int)((col % RS) / D)];
-      x = fma(-cq.x, rq.y, x);
-      x = fma(-rq.x, cq.y, x);
-    }
-    const double v = fma(x * xc.z, rowq[(int)(it & (C2 - 1))].z, 2.0);
-    best = v > best ? v : best;
-  }
-  return best;
-}
-template <int D>
-__device__ __forceinline__ ColState<D> col_state(const double (&cov)[D], const int (&lim)[D]) {
-  ColState<D> st;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    st.cov[d] = cov[d];
-    st.lim[d] = lim[d];
-  }
-  return st;
-}
-
 // One rotation: D consecutive rows ib .. ib+D-1 (processed as D/2 row pairs) of this thread's D
 // diagonals.  X[(u + d) % D] holds the operands of column ib + u + dt + d at row ib + u.
-template <typename T, int D, int RSD, bool MASKED, int C2>
-__device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D], T (&CK)[D], int (&CKh)[D],
+template <typename T, int D, int RSD, bool MASKED>
+__device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D], T (&CK)[D],
                                          const typename JT<T>::Q* rowp,
                                          const typename JT<T>::Q* ring0,
                                          const typename JT<T>::Q* ring1,
                                          const T* cth0, typename JT<T>::Q* rowq, T* cthr, int rb, int qt,
                                          int64_t ib, int64_t dt, const int (&lim)[D],
-                                         int64_t* keys, int64_t* keysc, int64_t i0, const typename JT<T>::Q* ring) {
-  constexpr bool HI = sizeof(T) == 8 && SKMP_F64_HI && SKMP_F64_COLHI;
+                                         int64_t* keys, int64_t* keysc) {
   using Q = typename JT<T>::Q;
 #pragma unroll
   for (int u = 0; u < D; u += 2) {
@@ -183,7 +114,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
       const Q& x = X[(u + d) % D];
       cov[d] = fma(ra.x, x.y, cov[d]);
       cov[d] = fma(x.x, ra.y, cov[d]);
-      ka[d] = fma(cov[d] * x.z, ra.z, rho_shift<T>());  // rho(i, j) = cov inv_j inv_i (+ shift)
+      ka[d] = (cov[d] * x.z) * ra.z;  // rho(i, j) = cov inv_j inv_i
     }
     if (MASKED) {
 #pragma unroll
@@ -191,10 +122,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     }
     // -- row u+1 (its entering column reuses the register of row u's completed column) --
     const Q rbq = rowp[u + 1];
-    T colv0;
-    int colh0 = 0;
-    if constexpr (HI) colh0 = max(CKh[u % D], hi_word(ka[0]));
-    else colv0 = max2(CK[u % D], ka[0]);  // column ib+u+dt completes after row u
+    const T colv0 = max2(CK[u % D], ka[0]);  // column ib+u+dt completes after row u
     X[u % D] = ring1[(u % D) * RSD];
     T kb[D];
 #pragma unroll
@@ -202,78 +130,30 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
       const Q& x = X[(u + 1 + d) % D];
       cov[d] = fma(rbq.x, x.y, cov[d]);
       cov[d] = fma(x.x, rbq.y, cov[d]);
-      kb[d] = fma(cov[d] * x.z, rbq.z, rho_shift<T>());
+      kb[d] = (cov[d] * x.z) * rbq.z;
     }
     if (MASKED) {
 #pragma unroll
       for (int d = 0; d < D; ++d) kb[d] = ((int)ib + u + 1 < lim[d]) ? kb[d] : neg_inf<T>();
     }
     // -- column maxima: registers x = (u + d) % D --
-    T colv1;
-    int colh1 = 0;
-    if constexpr (HI) {
-      colh1 = max(CKh[(u + 1) % D], max(hi_word(ka[1]), hi_word(kb[0])));
+    const T colv1 = max3(CK[(u + 1) % D], ka[1], kb[0]);  // column ib+u+1+dt completes
 #pragma unroll
-      for (int d = 2; d < D - 1; ++d)
-        CKh[(u + d) % D] = max(CKh[(u + d) % D], max(hi_word(ka[d]), hi_word(kb[d - 1])));
-      CKh[(u + D - 1) % D] = max(hi_word(ka[D - 1]), hi_word(kb[D - 2]));
-      CKh[u % D] = hi_word(kb[D - 1]);
-    } else {
-      colv1 = max3(CK[(u + 1) % D], ka[1], kb[0]);  // column ib+u+1+dt completes
-#pragma unroll
-      for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = max3(CK[(u + d) % D], ka[d], kb[d - 1]);
-      CK[(u + D - 1) % D] = max2(ka[D - 1], kb[D - 2]);  // column entered at row u
-      CK[u % D] = kb[D - 1];                              // column entered at row u+1
-    }
+    for (int d = 2; d < D - 1; ++d) CK[(u + d) % D] = max3(CK[(u + d) % D], ka[d], kb[d - 1]);
+    CK[(u + D - 1) % D] = max2(ka[D - 1], kb[D - 2]);  // column entered at row u
+    CK[u % D] = kb[D - 1];                              // column entered at row u+1
+    // -- row maxima over the D slots --
+    const T rowa = tree_max<T, D>(ka);
+    const T rowb = tree_max<T, D>(kb);
     // -- check-then-publish (rare) --
     // row thresholds ride in the row records' 4th word (ra.w, rbq.w): no extra loads
     // ">=": a candidate EQUAL to the current best is published too, so exact ties always reach
     // the atomic (smallest set wins) and keys do not depend on the tile order / band split
-    if constexpr (HI) {
-      // row and column maxima on the high words as a filter; exact FP64 only on the rare path
-      int ha = hi_word(ka[0]), hb = hi_word(kb[0]);
-#pragma unroll
-      for (int d = 1; d < D; ++d) {
-        ha = max(ha, hi_word(ka[d]));
-        hb = max(hb, hi_word(kb[d]));
-      }
-      const int* ch = reinterpret_cast<const int*>(cth0);  // high words of the column thresholds
-      const bool hit = (ha >= hi_word(ra.w)) | (hb >= hi_word(rbq.w)) | (colh0 >= ch[2 * ((u % D) * RSD) + 1]) |
-                       (colh1 >= ch[2 * (((u + 1) % D) * RSD) + 1]);
-      if (__any_sync(0xffffffffu, hit)) {
-        const T rowa = tree_max<T, D>(ka);
-        const T rowb = tree_max<T, D>(kb);
-        const int64_t ir = ib + u + 1;  // cov[] holds this row
-        const T cv0 = col_exact<D, RSD, C2>(col_state<D>(cov, lim), ib + u + dt, ir, i0, dt, rowq, ring);
-        const T cv1 = col_exact<D, RSD, C2>(col_state<D>(cov, lim), ib + u + 1 + dt, ir, i0, dt, rowq, ring);
-        publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
-                           ib + u, dt, rowa, rowb, cv0, cv1);
-      }
-    } else if constexpr (sizeof(T) == 8 && SKMP_F64_HI) {
-      // row maxima on the high words as a filter, the exact maxima only on the rare path
-      int ha = hi_word(ka[0]), hb = hi_word(kb[0]);
-#pragma unroll
-      for (int d = 1; d < D; ++d) {
-        ha = max(ha, hi_word(ka[d]));
-        hb = max(hb, hi_word(kb[d]));
-      }
-      const bool hit = (ha >= hi_word(ra.w)) | (hb >= hi_word(rbq.w)) | (colv0 >= cth0[(u % D) * RSD]) |
-                       (colv1 >= cth0[((u + 1) % D) * RSD]);
-      if (__any_sync(0xffffffffu, hit)) {
-        const T rowa = tree_max<T, D>(ka);
-        const T rowb = tree_max<T, D>(kb);
-        publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
-                           ib + u, dt, rowa, rowb, colv0, colv1);
-      }
-    } else {
-      const T rowa = tree_max<T, D>(ka);
-      const T rowb = tree_max<T, D>(kb);
-      const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
-                       (colv1 >= cth0[((u + 1) % D) * RSD]);
-      if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
-        publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
-                           ib + u, dt, rowa, rowb, colv0, colv1);
-      }
+    const bool hit = (rowa >= ra.w) | (rowb >= rbq.w) | (colv0 >= cth0[(u % D) * RSD]) |
+                     (colv1 >= cth0[((u + 1) % D) * RSD]);
+    if (__any_sync(0xffffffffu, hit)) {  // warp-uniform branch: no reconvergence stack
+      publish_pair<T, D>(keys, keysc, rowq, cthr, rb + u, (u % D) * RSD + qt, ((u + 1) % D) * RSD + qt,
+                         ib + u, dt, rowa, rowb, colv0, colv1);
     }
   }
 }
@@ -356,7 +236,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int e = tid; e < W + C; e += NT) {
     const int64_t c = i0 + delta0 + e;
     stage_q<T>(&ring[G::pos(c)], &qc[c]);
-    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
+    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
   }
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
@@ -366,7 +246,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // row thresholds go into the staged row records' 4th word once the copies have landed
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
-    rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
+    rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
   }
   __syncthreads();  // (one warp per CTA: a warp barrier; kept generic for NT > 32)
 
@@ -375,12 +255,8 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #pragma unroll
   for (int d = 0; d < D - 1; ++d) X[d] = ring[G::pos(i0 + dt + d)];
   T CK[D];  // running column maxima, same rotation as X
-  int CKh[D];  // ... their high words (FP64 with SKMP_F64_COLHI)
 #pragma unroll
-  for (int d = 0; d < D; ++d) {
-    CK[d] = neg_inf<T>();
-    CKh[d] = INT_MIN;
-  }
+  for (int d = 0; d < D; ++d) CK[d] = neg_inf<T>();
 
   // ring row index of column (ib + dt): qt; (ib + dt) is a multiple of D
   int qt = (int)(((i0 + dt) % RS) / D);
@@ -393,21 +269,17 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     constexpr int CPT = C / NT;
     static_assert(C % NT == 0, "chunk rows must be a multiple of the CTA size");
     T nthr_c[CPT], nthr_r[CPT];
-    // issued after the chunk's first rotation: until then the previous chunk's last rows and
-    // columns (the slots the prefetch overwrites) may still be read (SKMP_F64_COLHI back-steps)
-    auto prefetch = [&]() {
-      if (more) {
+    if (more) {
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) {
-          const int64_t nc = r + delta0 + W + C + tid + e * NT;
-          stage_q<T>(&ring[G::pos(nc)], &qc[nc]);
-          nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
-          const int64_t nr = r + C + tid + e * NT;
-          stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
-          nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) + rho_shift<T>() : pos_inf<T>();
-        }
+      for (int e = 0; e < CPT; ++e) {
+        const int64_t nc = r + delta0 + W + C + tid + e * NT;
+        stage_q<T>(&ring[G::pos(nc)], &qc[nc]);
+        nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) : pos_inf<T>();
+        const int64_t nr = r + C + tid + e * NT;
+        stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
+        nthr_r[e] = (nr < n_sub) ? load_thr(keys, nr, (T*)nullptr) : pos_inf<T>();
       }
-    };
+    }
 
     // ---- compute rows [r, rend) in D-row rotations of 2-row pairs ---------------------------
     // 32-bit bookkeeping only: rb = ib mod 2C (row buffer), qt = ring row of column ib + dt.
@@ -420,16 +292,14 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation<T, D, RSD, true, 2 * C>(cov, X, CK, CKh, rowq + rb, ring + qt, ring + qt1, cthr + qt,
-                                         rowq, cthr, rb, qt, ib, dt, lim, keys, keysc, i0, ring);
+        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+                                  rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       else
-        rotation<T, D, RSD, false, 2 * C>(cov, X, CK, CKh, rowq + rb, ring + qt, ring + qt1, cthr + qt,
-                                          rowq, cthr, rb, qt, ib, dt, lim, keys, keysc, i0, ring);
+        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+                                   rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       qt = qt1;
       rb = (rb + D) & (2 * C - 1);
-      if (it == 0) prefetch();
     }
-    if (nrot == 0) prefetch();
 
     // ---- land the prefetched chunk (row thresholds after the row copies landed) --------------
     cp_async_wait_all();
@@ -448,26 +318,17 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // x = d - 1 holds column i1 + dt + x.
 #pragma unroll
   for (int x = 0; x < D - 1; ++x) {
+    const T v = CK[x];
     const int64_t c = i1 + dt + x;
-    T v = CK[x];
-    if constexpr (sizeof(T) == 8 && SKMP_F64_HI && SKMP_F64_COLHI) {
-      if (c < n_sub_c && CKh[x] >= reinterpret_cast<const int*>(&cthr[G::pos(c)])[1])
-        v = col_exact<D, RSD, 2 * C>(col_state<D>(cov, lim), c, i1 - 1, i0, dt, rowq, ring);
-      else
-        v = neg_inf<T>();
-    }
-    if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v - rho_shift<T>(), c - dt - (D - 1));
+    if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v, c - dt - (D - 1));
   }
 }
 
-#ifndef SKMP_JOIN_MINB64
-#define SKMP_JOIN_MINB64 16  // FP64 D=4 with the high-word filters: <= 128 registers
-#endif
 #ifndef SKMP_JOIN_MINB
 #define SKMP_JOIN_MINB 20  // FP32 D=8: cap at ~96 registers -> 20 warps/SM (measured best)
 #endif
 template <typename T, int D, int NT, int C>
-__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : SKMP_JOIN_MINB64))
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : 1))
 join_kernel(JoinArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = NT * D;
