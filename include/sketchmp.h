@@ -171,7 +171,7 @@ void sketch_free_async(skmp_sketch* h, void* stream);
 typedef struct {
   int32_t m;            /* subsequence length, >= 2                                          */
   int32_t excl;         /* exclusion radius; < 0 -> ceil(m/2)                                 */
-  int32_t reseed_rows;  /* 0 -> default (FP32 16384, FP64 2048); rounded up to 64             */
+  int32_t reseed_rows;  /* 0 -> default (FP32 16384, or 32768 from 2^20 windows; FP64 2048); rounded up to 64 */
   int32_t reserved;     /* must be 0                                                          */
 } skmp_mp_cfg;
 

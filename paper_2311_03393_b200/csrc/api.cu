@@ -759,7 +759,12 @@ skmp_status mp_create_impl(const void* R, int32_t k, int64_t n, int64_t ld, int3
   w.excl = excl;
   w.n_sub = n - cfg->m + 1;
   w.ldq = round_up(w.n_sub + join_pad(dtype), 64);
-  int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows : (dtype == SKMP_F32 ? 16384 : 2048);
+  // FP32 re-seed interval: 16,384 rows; 32,768 for series of >= 2^20 windows, where the longer
+  // tiles amortise the seeds better (measured: C5-length join 1683 -> 1676 ms; at C4 size the
+  // longer tiles were slower, 283 -> 287 ms).  FP32 rho drift stays ~1e-5; P is
+  // resolved exactly in FP64 by the finalize either way.
+  int L0 = cfg->reseed_rows > 0 ? cfg->reseed_rows
+                                : (dtype == SKMP_F32 ? ((n - cfg->m + 1) >= (1 << 20) ? 32768 : 16384) : 2048);
   if (cfg->reseed_rows <= 0) {
     // small problems: shorten the tiles until the grid has ~2 waves of 148 SMs x 16 warps
     const int64_t W = join_width(dtype);
