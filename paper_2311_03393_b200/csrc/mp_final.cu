@@ -52,8 +52,8 @@ __device__ __forceinline__ int64_t smallest_adm_flat(const int32_t* F, int32_t n
 
 // Transposed warp sum of N per-lane values: afterwards every lane holds in v[0] the warp total
 // of value xidx<N>(lane) (log2(N) exchange steps keep half the values each, then plain steps).
-template <int N, typename V>
-__device__ __forceinline__ void xsum(V (&v)[N], int lane) {
+template <int N>
+__device__ __forceinline__ void xsum(double (&v)[N], int lane) {
   int c = N;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -62,8 +62,8 @@ __device__ __forceinline__ void xsum(V (&v)[N], int lane) {
 #pragma unroll
       for (int q = 0; q < N / 2; ++q) {
         if (q < c / 2) {
-          const V send = up ? v[q] : v[q + c / 2];
-          const V keep = up ? v[q + c / 2] : v[q];
+          const double send = up ? v[q] : v[q + c / 2];
+          const double keep = up ? v[q + c / 2] : v[q];
           v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
       }
@@ -298,12 +298,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 constexpr int kFinRegWarps = 4;
-// FP32 configurations rank a key's candidate set in FP32 and compute only the chosen member in
-// FP64 (SKMP_FIN_SEL32=0: the whole set in FP64, as for FP64 configurations)
-#ifndef SKMP_FIN_SEL32
-#define SKMP_FIN_SEL32 1
-#endif
-template <typename T> constexpr bool kSel32 = (sizeof(T) == 4) && SKMP_FIN_SEL32;
 // squared distances below this are recomputed by explicit differences (the dot-product form
 // 2m - 2 cov / (sigma_i sigma_j) loses ~1e-14 absolute to cancellation: at dd >= 1 that is
 // < 1e-13 relative in P, far inside the 1e-9 FP64 bar; near-duplicate windows need the
@@ -389,7 +383,7 @@ __device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64
   return p;
 }
 
-template <typename T, int SPAN, int E, bool FULL, bool SEL32>
+template <typename T, int SPAN, int E, bool FULL>
 __global__ void __launch_bounds__(32 * kFinRegWarps)
 finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
                     int64_t* __restrict__ I) {
@@ -442,168 +436,78 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
     const bool has = key_arg(kw, words, &kb);
     const int64_t b = has ? kb : 0;
     const double mi = cu.mi;
+    // ---- the SPAN candidate dot products, in registers --------------------------------------
     const T* xi = cur;
     const T* xo = cur + B::XI;
-    int d;
-    int64_t jr;
-    double pe, mj;
-    bool fj;
-    if constexpr (SEL32) {
-      // ---- FP32 configurations: the SPAN candidates ranked in FP32 (FP32 products of the staged
-      // values, both sides centred — the candidates by the first member's mean — so no digits are
-      // lost to a window offset), then the chosen member's dot product in FP64 ------------------
-      const double mb = __shfl_sync(0xffffffffu, cu.mc, 0);  // lane 0 prefetched candidate 0
-      const float mi32 = (float)mi, mb32 = (float)mb;
-      float a32[E], w32[E + SPAN - 1];
+    double a[E], wv[E + SPAN - 1];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int s = E * lane + e;
-        a32[e] = (FULL || s < m) ? (float)xi[pad_pos<E>(s)] - mi32 : 0.0f;
-      }
+    for (int e = 0; e < E; ++e) {
+      const int s = E * lane + e;
+      a[e] = (FULL || s < m) ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
+    }
 #pragma unroll
-      for (int t = 0; t < E + SPAN - 1; ++t) w32[t] = (float)xo[pad_pos<E>(E * lane + t)] - mb32;
-      float acc32[SPAN], asum32 = 0.0f;
+    for (int t = 0; t < E + SPAN - 1; ++t) wv[t] = (double)xo[pad_pos<E>(E * lane + t)];
+    double acc[SPAN], asum = 0.0;
 #pragma unroll
-      for (int dd_ = 0; dd_ < SPAN; ++dd_) acc32[dd_] = 0.0f;
+    for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        asum32 += a32[e];
+    for (int e = 0; e < E; ++e) {
+      asum += a[e];
 #pragma unroll
-        for (int dd_ = 0; dd_ < SPAN; ++dd_) acc32[dd_] = fmaf(a32[e], w32[e + dd_], acc32[dd_]);
-      }
+      for (int d = 0; d < SPAN; ++d) acc[d] = fma(a[e], wv[e + d], acc[d]);
+    }
 #pragma unroll
-      for (int q = 16; q > 0; q >>= 1) asum32 += __shfl_xor_sync(0xffffffffu, asum32, q);
-      xsum<SPAN>(acc32, lane);
-      d = xidx<SPAN>(lane);
-      float d32 = __int_as_float(0x7f800000);
-      if (admissible(i, b + d, wo.n_sub, excl)) {
-        if (cu.fc) {
-          d32 = (float)m;
-        } else {
-          const float cov = acc32[0] - (float)(cu.mc - mb) * asum32;
-          d32 = 2.0f * m - (2.0f * cov) * (float)(cu.ii * cu.ic);
-        }
-      }
-#pragma unroll
-      for (int q = 16; q >= 32 / SPAN; q >>= 1) {
-        const float od = __shfl_xor_sync(0xffffffffu, d32, q);
-        const int oi = __shfl_xor_sync(0xffffffffu, d, q);
-        if (od < d32 || (od == d32 && oi < d)) {
-          d32 = od;
-          d = oi;
-        }
-      }
-      jr = d32 < __int_as_float(0x7f800000) ? b + d : -1;
-      const int src = xlane<SPAN>(jr >= 0 ? d : 0);
-      mj = __shfl_sync(0xffffffffu, cu.mc, src);
-      const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
-      fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
-      // the chosen member in FP64: centred dot product -> dd, P = sqrt(dd); a near neighbour
-      // (dd < 1) by explicit differences (Def. 3)
-      const bool exact = jr >= 0 && !fj;
-      const int de = exact ? d : 0;
-      double a64[E], acc = 0.0, asum = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int s = E * lane + e;
-        a64[e] = (FULL || s < m) ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
-        asum += a64[e];
-        acc = fma(a64[e], (double)xo[pad_pos<E>(s + de)], acc);
-      }
-#pragma unroll
-      for (int q = 16; q > 0; q >>= 1) {
-        acc += __shfl_xor_sync(0xffffffffu, acc, q);
-        asum += __shfl_xor_sync(0xffffffffu, asum, q);
-      }
-      const double dd = 2.0 * m - (2.0 * (acc - mj * asum)) * (cu.ii * ij);
-      pe = sqrt(dd > 0.0 ? dd : 0.0);
-      if (exact && dd < kFinExplicitBelow) {
-        const double ii = cu.ii;
-        double acc2 = 0.0;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int s = E * lane + e;
-          const double zi = __dmul_rn(a64[e], ii);
-          const double zj = __dmul_rn((double)xo[pad_pos<E>(s + de)] - mj, ij);
-          const double df = zi - zj;
-          acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
-        }
-#pragma unroll
-        for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
-        pe = sqrt(acc2);
-      }
-    } else {
-      double a[E], wv[E + SPAN - 1];
-  #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int s = E * lane + e;
-        a[e] = (FULL || s < m) ? (double)xi[pad_pos<E>(s)] - mi : 0.0;
-      }
-  #pragma unroll
-      for (int t = 0; t < E + SPAN - 1; ++t) wv[t] = (double)xo[pad_pos<E>(E * lane + t)];
-      double acc[SPAN], asum = 0.0;
-  #pragma unroll
-      for (int q = 0; q < SPAN; ++q) acc[q] = 0.0;
-  #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        asum += a[e];
-  #pragma unroll
-        for (int q = 0; q < SPAN; ++q) acc[q] = fma(a[e], wv[e + q], acc[q]);
-      }
-  #pragma unroll
-      for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
-      xsum<SPAN>(acc, lane);
-      d = xidx<SPAN>(lane);
-      double dd = inf;
-      const int64_t jd = b + d;
-      if (admissible(i, jd, wo.n_sub, excl)) {
-        if (cu.fc) {
-          dd = (double)m;
-        } else {
-          const double cov = acc[0] - cu.mc * asum;
-          dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
-        }
-      }
-      // argmin over the SPAN candidates: the 32 / SPAN lanes of a candidate hold the same value
-      // (xidx ignores the low lane bits), so only the high log2(SPAN) butterfly rounds are needed
-  #pragma unroll
-      for (int q = 16; q >= 32 / SPAN; q >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, dd, q);
-        const int oi = __shfl_xor_sync(0xffffffffu, d, q);
-        if (od < dd || (od == dd && oi < d)) {
-          dd = od;
-          d = oi;
-        }
-      }
-      jr = dd < inf ? b + d : -1;
-      // the chosen member's statistics from the lane that prefetched them
-      const int src = xlane<SPAN>(jr >= 0 ? d : 0);
-      mj = __shfl_sync(0xffffffffu, cu.mc, src);
-      const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
-      fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
-      // ---- the chosen member's distance: sqrt(dd) from the centred FP64 dot product, and for a
-      // near neighbour (dd < 1, where the cancellation in 2m - 2 cov / (sigma sigma) would show)
-      // recomputed by explicit differences (Def. 3); warp-uniform branch ------------------------
-      const bool exact = jr >= 0 && !fj;
-      const int de = exact ? d : 0;
-      pe = sqrt(dd > 0.0 ? dd : 0.0);
-      if (exact && dd < kFinExplicitBelow) {
-        const double ii = cu.ii;
-        double acc2 = 0.0;
-  #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int s = E * lane + e;
-          const double zi = __dmul_rn(a[e], ii);
-          const double zj = __dmul_rn((double)xo[pad_pos<E>(s + de)] - mj, ij);
-          const double df = zi - zj;
-          acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
-        }
-  #pragma unroll
-        for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
-        pe = sqrt(acc2);
+    for (int q = 16; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+    xsum<SPAN>(acc, lane);
+    int d = xidx<SPAN>(lane);
+    double dd = inf;
+    const int64_t jd = b + d;
+    if (admissible(i, jd, wo.n_sub, excl)) {
+      if (cu.fc) {
+        dd = (double)m;
+      } else {
+        const double cov = acc[0] - cu.mc * asum;
+        dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
       }
     }
+    // argmin over the SPAN candidates: the 32 / SPAN lanes of a candidate hold the same value
+    // (xidx ignores the low lane bits), so only the high log2(SPAN) butterfly rounds are needed
+#pragma unroll
+    for (int q = 16; q >= 32 / SPAN; q >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, dd, q);
+      const int oi = __shfl_xor_sync(0xffffffffu, d, q);
+      if (od < dd || (od == dd && oi < d)) {
+        dd = od;
+        d = oi;
+      }
+    }
+    const int64_t jr = dd < inf ? b + d : -1;
+    // the chosen member's statistics from the lane that prefetched them
+    const int src = xlane<SPAN>(jr >= 0 ? d : 0);
+    const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
+    const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
+    const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
+    // ---- the chosen member's distance: sqrt(dd) from the centred FP64 dot product, and for a
+    // near neighbour (dd < 1, where the cancellation in 2m - 2 cov / (sigma sigma) would show)
+    // recomputed by explicit differences (Def. 3); warp-uniform branch ------------------------
     const bool exact = jr >= 0 && !fj;
+    const int de = exact ? d : 0;
+    double pe = sqrt(dd > 0.0 ? dd : 0.0);
+    if (exact && dd < kFinExplicitBelow) {
+      const double ii = cu.ii;
+      double acc2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int s = E * lane + e;
+        const double zi = __dmul_rn(a[e], ii);
+        const double zj = __dmul_rn((double)xo[pad_pos<E>(s + de)] - mj, ij);
+        const double df = zi - zj;
+        acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
+      }
+#pragma unroll
+      for (int q = 16; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+      pe = sqrt(acc2);
+    }
     double p;
     int64_t j;
     if (cu.fi) {
@@ -664,9 +568,9 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
 #define SKMP_FINR(TT, SP, EE)                                                                                    \
   do {                                                                                                          \
     if (w.m == 32 * (EE))                                                                                       \
-      finalize_reg_kernel<TT, SP, EE, true, kSel32<TT>><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+      finalize_reg_kernel<TT, SP, EE, true><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
     else                                                                                                        \
-      finalize_reg_kernel<TT, SP, EE, false, kSel32<TT>><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+      finalize_reg_kernel<TT, SP, EE, false><<<grid, ntr, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
   } while (0)
     if (w.span == 8) {
       if (E == 2) { if (f32) SKMP_FINR(float, 8, 2); else SKMP_FINR(double, 8, 2); }
