@@ -298,6 +298,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 constexpr int kFinRegWarps = 4;
+#ifndef SKMP_FIN_MINB
+#define SKMP_FIN_MINB 1  // resident CTAs the register allocation must allow (A/B: 6, 8)
+#endif
 // squared distances below this are recomputed by explicit differences (the dot-product form
 // 2m - 2 cov / (sigma_i sigma_j) loses ~1e-14 absolute to cancellation: at dd >= 1 that is
 // < 1e-13 relative in P, far inside the 1e-9 FP64 bar; near-duplicate windows need the
@@ -384,7 +387,7 @@ __device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64
 }
 
 template <typename T, int SPAN, int E, bool FULL>
-__global__ void __launch_bounds__(32 * kFinRegWarps)
+__global__ void __launch_bounds__(32 * kFinRegWarps, SKMP_FIN_MINB)
 finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
                     int64_t* __restrict__ I) {
   static_assert(SPAN <= 32 && (SPAN & (SPAN - 1)) == 0 && (E % 2) == 0, "geometry");
