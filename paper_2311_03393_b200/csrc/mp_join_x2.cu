@@ -431,46 +431,94 @@ join_x2_kernel(JoinArgs a) {
     const double* mu = a.mu + (int64_t)g * a.ldq;
     const double* muc = a.muc + (int64_t)g * a.ldqc;
     const double mua = mu[i0];
-    double acc[2 * DG], mub[2 * DG];
+    double acc[2 * DG];
 #pragma unroll
-    for (int e = 0; e < 2 * DG; ++e) {
-      const int64_t j = i0 + dt + (e % DG) + (e >= DG ? H : 0);
-      mub[e] = (j < n_sub_c) ? muc[j] : 0.0;
-      acc[e] = 0.0;
-    }
-    // column samples through two register rings (group A at jb, group B at jb + H): sample
-    // jb + s + d sits in slot (s + d) % DG, so each sample is loaded and converted once per
-    // thread instead of once per diagonal
+    for (int e = 0; e < 2 * DG; ++e) acc[e] = 0.0;
     const int64_t jb = i0 + dt;
-    double wa[DG], wb[DG];
-#pragma unroll
-    for (int d = 0; d < DG - 1; ++d) {
-      wa[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
-      wb[d] = (jb + H + d < a.nc) ? (double)Rc[jb + H + d] : 0.0;
-    }
     // sum_s (R_i - mu_i)(R_j - mu_j) = sum_s (R_i - mu_i) R_j - mu_j sum_s (R_i - mu_i): one FP64 FMA
     // per term instead of a subtraction and an FMA (the seeds are rounded to FP32 afterwards)
     double asum = 0.0;
-    for (int s0 = 0; s0 < a.m; s0 += DG) {
+    // fast path (every tile but those at a series' end): 16-byte aligned windows wholly inside
+    // both series and m a multiple of DG -- the samples arrive as float4 loads, each DG-sample
+    // step's loads issued one step ahead, column samples in a 2 DG register window
+    const bool vec = ((reinterpret_cast<uintptr_t>(R + i0) | reinterpret_cast<uintptr_t>(Rc + jb)) & 15) == 0 &&
+                     (a.m % DG) == 0 && a.m >= 2 * DG && jb + H + a.m + DG <= a.nc;
+    if (__all_sync(0xffffffffu, vec)) {
+      const float4* r4 = reinterpret_cast<const float4*>(R + i0);
+      const float4* ca = reinterpret_cast<const float4*>(Rc + jb);
+      const float4* cb = reinterpret_cast<const float4*>(Rc + jb + H);
+      double wa[2 * DG], wb[2 * DG];
+      auto put = [](double* w, float4 x, float4 y) {
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w; w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
+      };
+      static_assert(DG == 8, "float4 seed path is written for DG = 8");
+      put(wa, ca[0], ca[1]);
+      put(wb, cb[0], cb[1]);
+      float4 na0 = ca[2], na1 = ca[3], nb0 = cb[2], nb1 = cb[3], nr0 = r4[0], nr1 = r4[1];
+      for (int s0 = 0; s0 < a.m; s0 += DG) {
+        put(wa + DG, na0, na1);
+        put(wb + DG, nb0, nb1);
+        double av[DG];
+        put(av, nr0, nr1);
+        if (s0 + DG < a.m) {  // the next step's samples, in flight during this step's FMAs
+          const int q = (s0 + 2 * DG) >> 2;
+          na0 = ca[q];
+          na1 = ca[q + 1];
+          nb0 = cb[q];
+          nb1 = cb[q + 1];
+          nr0 = r4[(s0 + DG) >> 2];
+          nr1 = r4[((s0 + DG) >> 2) + 1];
+        }
 #pragma unroll
-      for (int u = 0; u < DG; ++u) {
-        const int s = s0 + u;
-        if (s < a.m) {
-          const int64_t t = jb + s + DG - 1;
-          wa[(u + DG - 1) % DG] = (t < a.nc) ? (double)Rc[t] : 0.0;
-          wb[(u + DG - 1) % DG] = (t + H < a.nc) ? (double)Rc[t + H] : 0.0;
-          const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
-          asum += av;
+        for (int u = 0; u < DG; ++u) {
+          const double x = av[u] - mua;
+          asum += x;
 #pragma unroll
           for (int d = 0; d < DG; ++d) {
-            acc[d] = fma(av, wa[(u + d) % DG], acc[d]);
-            acc[DG + d] = fma(av, wb[(u + d) % DG], acc[DG + d]);
+            acc[d] = fma(x, wa[u + d], acc[d]);
+            acc[DG + d] = fma(x, wb[u + d], acc[DG + d]);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < DG; ++t) {
+          wa[t] = wa[t + DG];
+          wb[t] = wb[t + DG];
+        }
+      }
+    } else {
+      // column samples through two register rings (group A at jb, group B at jb + H): sample
+      // jb + s + d sits in slot (s + d) % DG, so each sample is loaded and converted once per
+      // thread instead of once per diagonal
+      double wa[DG], wb[DG];
+#pragma unroll
+      for (int d = 0; d < DG - 1; ++d) {
+        wa[d] = (jb + d < a.nc) ? (double)Rc[jb + d] : 0.0;
+        wb[d] = (jb + H + d < a.nc) ? (double)Rc[jb + H + d] : 0.0;
+      }
+      for (int s0 = 0; s0 < a.m; s0 += DG) {
+#pragma unroll
+        for (int u = 0; u < DG; ++u) {
+          const int s = s0 + u;
+          if (s < a.m) {
+            const int64_t t = jb + s + DG - 1;
+            wa[(u + DG - 1) % DG] = (t < a.nc) ? (double)Rc[t] : 0.0;
+            wb[(u + DG - 1) % DG] = (t + H < a.nc) ? (double)Rc[t + H] : 0.0;
+            const double av = (i0 + s < a.n) ? (double)R[i0 + s] - mua : 0.0;
+            asum += av;
+#pragma unroll
+            for (int d = 0; d < DG; ++d) {
+              acc[d] = fma(av, wa[(u + d) % DG], acc[d]);
+              acc[DG + d] = fma(av, wb[(u + d) % DG], acc[DG + d]);
+            }
           }
         }
       }
     }
 #pragma unroll
-    for (int e = 0; e < 2 * DG; ++e) acc[e] = fma(-mub[e], asum, acc[e]);
+    for (int e = 0; e < 2 * DG; ++e) {  // the column windows' means, loaded after the sums (registers)
+      const int64_t j = i0 + dt + (e % DG) + (e >= DG ? H : 0);
+      acc[e] = fma(-((j < n_sub_c) ? muc[j] : 0.0), asum, acc[e]);
+    }
     const float4 qi = q[i0];
     float c32[2 * DG];
 #pragma unroll
