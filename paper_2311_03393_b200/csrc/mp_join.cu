@@ -92,13 +92,49 @@ __device__ __forceinline__ void stage_q(typename JT<T>::Q* dst, const typename J
     cp_async16(reinterpret_cast<char*>(dst) + 16 * q, reinterpret_cast<const char*>(src) + 16 * q);
 }
 
+// The column ring in shared memory.  FP32 records (float4, 16 B) are read whole by consecutive
+// lanes (conflict-free 128-bit loads); an FP64 record is 32 B, and lanes reading whole 32-B
+// records hit every bank twice per 128-bit load (2x the wavefronts: 2.5e10 shared-load bank
+// conflicts per FP64 n=2e5 join, short-scoreboard stalls 1.1 per issue), so FP64 records are
+// split into two 16-B halves in two arrays, each read conflict-free.
+template <typename T> struct RingView {
+  typename JT<T>::Q* q;
+  __device__ __forceinline__ typename JT<T>::Q load(int p) const { return q[p]; }
+  __device__ __forceinline__ void stage(int p, const typename JT<T>::Q* src) const { stage_q<T>(&q[p], src); }
+};
+template <> struct RingView<double> {
+  double2* h0;  // {df, dg} of ring slot p
+  double2* h1;  // {inv, -}
+  __device__ __forceinline__ dq4 load(int p) const {
+    const double2 a = h0[p], b = h1[p];
+    dq4 r;
+    r.x = a.x;
+    r.y = a.y;
+    r.z = b.x;
+    r.w = b.y;
+    return r;
+  }
+  __device__ __forceinline__ void stage(int p, const dq4* src) const {
+    cp_async16(&h0[p], src);
+    cp_async16(&h1[p], reinterpret_cast<const char*>(src) + 16);
+  }
+};
+template <typename T, int RS>
+__device__ __forceinline__ RingView<T> ring_view(typename JT<T>::Q* base) {
+  if constexpr (sizeof(T) == 8) {
+    double2* h = reinterpret_cast<double2*>(base);
+    return RingView<double>{h, h + RS};
+  } else {
+    return RingView<T>{base};
+  }
+}
+
 // One rotation: D consecutive rows ib .. ib+D-1 (processed as D/2 row pairs) of this thread's D
 // diagonals.  X[(u + d) % D] holds the operands of column ib + u + dt + d at row ib + u.
 template <typename T, int D, int RSD, bool MASKED>
 __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D], T (&CK)[D],
                                          const typename JT<T>::Q* rowp,
-                                         const typename JT<T>::Q* ring0,
-                                         const typename JT<T>::Q* ring1,
+                                         RingView<T> rv, int p0, int p1,
                                          const T* cth0, typename JT<T>::Q* rowq, T* cthr, int rb, int qt,
                                          int64_t ib, int64_t dt, const int (&lim)[D],
                                          int64_t* keys, int64_t* keysc) {
@@ -107,7 +143,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
   for (int u = 0; u < D; u += 2) {
     // -- row u --
     const Q ra = rowp[u];
-    X[(u + D - 1) % D] = (u == 0) ? ring0[((u + D - 1) % D) * RSD] : ring1[((u + D - 1) % D) * RSD];
+    X[(u + D - 1) % D] = rv.load(((u + D - 1) % D) * RSD + (u == 0 ? p0 : p1));
     T ka[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -123,7 +159,7 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
     // -- row u+1 (its entering column reuses the register of row u's completed column) --
     const Q rbq = rowp[u + 1];
     const T colv0 = max2(CK[u % D], ka[0]);  // column ib+u+dt completes after row u
-    X[u % D] = ring1[(u % D) * RSD];
+    X[u % D] = rv.load((u % D) * RSD + p1);
     T kb[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -167,6 +203,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   constexpr int RS = G::RS;
   constexpr int RSD = G::RSD;
   Q* ring = reinterpret_cast<Q*>(smem_raw);
+  const RingView<T> rv = ring_view<T, RS>(ring);
   Q* rowq = ring + RS;
   T* cthr = reinterpret_cast<T*>(rowq + 2 * C);
 
@@ -235,7 +272,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // ---- prologue: stage rows [i0, i0+C) and ring columns [i0+delta0, i0+delta0+W+C) ----------
   for (int e = tid; e < W + C; e += NT) {
     const int64_t c = i0 + delta0 + e;
-    stage_q<T>(&ring[G::pos(c)], &qc[c]);
+    rv.stage(G::pos(c), &qc[c]);
     cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
   }
   for (int e = tid; e < C; e += NT) {
@@ -253,7 +290,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // column operand registers: X[(u + d) % D] holds column i + dt + d at unrolled row u
   Q X[D];
 #pragma unroll
-  for (int d = 0; d < D - 1; ++d) X[d] = ring[G::pos(i0 + dt + d)];
+  for (int d = 0; d < D - 1; ++d) X[d] = rv.load(G::pos(i0 + dt + d));
   T CK[D];  // running column maxima, same rotation as X
 #pragma unroll
   for (int d = 0; d < D; ++d) CK[d] = neg_inf<T>();
@@ -273,7 +310,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #pragma unroll
       for (int e = 0; e < CPT; ++e) {
         const int64_t nc = r + delta0 + W + C + tid + e * NT;
-        stage_q<T>(&ring[G::pos(nc)], &qc[nc]);
+        rv.stage(G::pos(nc), &qc[nc]);
         nthr_c[e] = (nc < n_sub_c) ? load_thr(keysc, nc, (T*)nullptr) : pos_inf<T>();
         const int64_t nr = r + C + tid + e * NT;
         stage_q<T>(&rowq[nr % (2 * C)], &q[nr]);
@@ -292,10 +329,10 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
       if (cmasked)
-        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
                                   rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       else
-        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, ring + qt, ring + qt1, cthr + qt,
+        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
                                    rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
       qt = qt1;
       rb = (rb + D) & (2 * C - 1);
