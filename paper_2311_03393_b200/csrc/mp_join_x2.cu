@@ -151,7 +151,15 @@ struct ColMax {
 // {e, o, e} / {o, e, o} triples, the second level's inputs are forced to opposite parities by
 // packing them as pairs
 __device__ __forceinline__ float row_max_bal(const float (&ka)[DG], const float (&kb)[DG]) {
-  static_assert(DG == 8, "balanced row tree is written for DG = 8");
+  if constexpr (DG != 8) {  // generic: interleaved {a, b, a}, {b, a, b} triples at the first level
+    float v[2 * DG];
+#pragma unroll
+    for (int d = 0; d < DG; ++d) {
+      v[2 * d] = ka[d];
+      v[2 * d + 1] = kb[d];
+    }
+    return tree_max<float, 2 * DG>(v);
+  }
   const float t0 = max3(ka[0], kb[0], ka[1]), t1 = max3(kb[1], ka[2], kb[2]);
   const float t2 = max3(ka[3], kb[3], ka[4]), t3 = max3(kb[4], ka[5], kb[5]);
   const float t4 = max3(ka[6], kb[6], ka[7]);
@@ -443,7 +451,9 @@ join_x2_kernel(JoinArgs a) {
     // step's loads issued one step ahead, column samples in a 2 DG register window
     const bool vec = ((reinterpret_cast<uintptr_t>(R + i0) | reinterpret_cast<uintptr_t>(Rc + jb)) & 15) == 0 &&
                      (a.m % DG) == 0 && a.m >= 2 * DG && jb + H + a.m + DG <= a.nc;
-    if (__all_sync(0xffffffffu, vec)) {
+    bool fast = false;
+    if constexpr (DG == 8) fast = __all_sync(0xffffffffu, vec);
+    if constexpr (DG == 8) if (fast) {
       const float4* r4 = reinterpret_cast<const float4*>(R + i0);
       const float4* ca = reinterpret_cast<const float4*>(Rc + jb);
       const float4* cb = reinterpret_cast<const float4*>(Rc + jb + H);
@@ -451,7 +461,7 @@ join_x2_kernel(JoinArgs a) {
       auto put = [](double* w, float4 x, float4 y) {
         w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w; w[4] = y.x; w[5] = y.y; w[6] = y.z; w[7] = y.w;
       };
-      static_assert(DG == 8, "float4 seed path is written for DG = 8");
+      // (DG = 8: two float4 per DG-sample step)
       put(wa, ca[0], ca[1]);
       put(wb, cb[0], cb[1]);
       float4 na0 = ca[2], na1 = ca[3], nb0 = cb[2], nb1 = cb[3], nr0 = r4[0], nr1 = r4[1];
@@ -485,7 +495,8 @@ join_x2_kernel(JoinArgs a) {
           wb[t] = wb[t + DG];
         }
       }
-    } else {
+    }
+    if (!fast) {
       // column samples through two register rings (group A at jb, group B at jb + H): sample
       // jb + s + d sits in slot (s + d) % DG, so each sample is loaded and converted once per
       // thread instead of once per diagonal
