@@ -87,8 +87,13 @@ struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 struct Smem {
   ColRec0 col0[RS];   // swizzled [DG][RSD]
   f2 col1[RS];        // {inv_c, inv_c+H}
+#if SKMP_X2_ROWSCALAR
+  float4 rowq[2 * C];  // raw row records {df, dg, inv, 0}; the f32x2 row operands are formed as
+                       // broadcasts {x, x}, which the FFMA2 / FMUL2 encode as .F32 scalar operands
+#else
   RowRec0 row0[2 * C];
   f2 row1[2 * C];     // {inv_i, inv_i}
+#endif
   float thrA[RS];     // column thresholds of group A columns (record base c)
   float thrB[RS];     // ... of group B columns (c + H)
   float rthr[2 * C];
@@ -130,6 +135,9 @@ struct Col {
 #endif
 #ifndef SKMP_X2_BAL
 #define SKMP_X2_BAL 1
+#endif
+#ifndef SKMP_X2_ROWSCALAR
+#define SKMP_X2_ROWSCALAR 1
 #endif
 #if SKMP_X2_BAL
 struct ColMax {
@@ -242,6 +250,15 @@ __device__ __forceinline__ void load_col(Col& x, const Smem* sm, int e) {
   x.inv = sm->col1[e];
 }
 
+#if SKMP_X2_ROWSCALAR
+__device__ __forceinline__ RowRec0 row0_of(const float4& r) { return RowRec0{pk(r.x, r.x), pk(r.y, r.y)}; }
+#define ROW0(e) row0_of(sm->rowq[(e)])
+#define ROW1(e) pk(sm->rowq[(e)].z, sm->rowq[(e)].z)
+#else
+#define ROW0(e) sm->row0[(e)]
+#define ROW1(e) sm->row1[(e)]
+#endif
+
 // One rotation = DG rows ib .. ib+DG-1 processed as DG/2 row pairs.  Column registers rotate:
 // X[(u + d) % DG] holds the record of column ib + u + dt + d (group A) / + H (group B).
 // CA/CB: running column maxima of the group A / B columns, same rotation.
@@ -254,14 +271,14 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], ColMax&
     // -- row u: its entering column (slot DG-1) takes the register of the column completed at u-1
     load_col(X[(u + DG - 1) % DG], sm, ((u + DG - 1) % DG) * RSD + (u == 0 ? qt : qt1));
     float ka[DG], kb[DG];
-    row_keys<MASKED>(u, cov, X, sm->row0[rb + u], sm->row1[rb + u], ka, kb, (int)ib + u, lim);
+    row_keys<MASKED>(u, cov, X, ROW0(rb + u), ROW1(rb + u), ka, kb, (int)ib + u, lim);
     // columns (ib+u)+dt (A) and +H (B) complete after row u
     const float cA0 = max2(CM.A(u % DG), ka[0]);
     const float cB0 = max2(CM.B(u % DG), kb[0]);
     // -- row u+1 --
     load_col(X[u % DG], sm, (u % DG) * RSD + qt1);
     float la[DG], lb[DG];
-    row_keys<MASKED>(u + 1, cov, X, sm->row0[rb + u + 1], sm->row1[rb + u + 1], la, lb,
+    row_keys<MASKED>(u + 1, cov, X, ROW0(rb + u + 1), ROW1(rb + u + 1), la, lb,
                      (int)ib + u + 1, lim);
     const float cA1 = max3(CM.A((u + 1) % DG), ka[1], la[0]);
     const float cB1 = max3(CM.B((u + 1) % DG), kb[1], lb[0]);
@@ -346,9 +363,13 @@ __device__ __forceinline__ void fetch_row(RowStage& s, const float4* q, const in
 }
 __device__ __forceinline__ void land_row(const RowStage& s, Smem* sm, int64_t i) {
   const int e = (int)(i & (2 * C - 1));
+#if SKMP_X2_ROWSCALAR
+  sm->rowq[e] = s.q;
+#else
   sm->row0[e].df = pk(s.q.x, s.q.x);
   sm->row0[e].dg = pk(s.q.y, s.q.y);
   sm->row1[e] = pk(s.q.z, s.q.z);
+#endif
   sm->rthr[e] = s.t;
 }
 
@@ -376,8 +397,11 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
   cp_async4(d0 + 3, b + 1);
   cp_async4(d1 + 0, a + 2);
   cp_async4(d1 + 1, b + 2);
-  const float* r = reinterpret_cast<const float*>(q + i);
   const int er = (int)(i & (2 * C - 1));
+#if SKMP_X2_ROWSCALAR
+  cp_async16(&sm->rowq[er], q + i);  // the raw record, one 16-byte copy
+#else
+  const float* r = reinterpret_cast<const float*>(q + i);
   float* r0 = reinterpret_cast<float*>(&sm->row0[er]);  // {df, df, dg, dg}
   float* r1 = reinterpret_cast<float*>(&sm->row1[er]);  // {inv, inv}
   cp_async4(r0 + 0, r + 0);
@@ -386,6 +410,7 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
   cp_async4(r0 + 3, r + 1);
   cp_async4(r1 + 0, r + 2);
   cp_async4(r1 + 1, r + 2);
+#endif
   const int32_t inf = 0x7f800000;  // orderable(+inf): never beaten
   if (c < nsc) cp_async4(&sm->rawtA[e], reinterpret_cast<const char*>(keysc + c) + 4); else sm->rawtA[e] = inf;
   if (c + H < nsc) cp_async4(&sm->rawtB[e], reinterpret_cast<const char*>(keysc + (c + H)) + 4); else sm->rawtB[e] = inf;
