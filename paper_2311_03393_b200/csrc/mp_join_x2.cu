@@ -81,6 +81,9 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
   return d;
 }
 
+#ifndef SKMP_X2_ROWSCALAR
+#define SKMP_X2_ROWSCALAR 1
+#endif
 struct __align__(16) ColRec0 { f2 df, dg; };   // {df_c, df_c+H}, {dg_c, dg_c+H}
 struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 
@@ -136,9 +139,7 @@ struct Col {
 #ifndef SKMP_X2_BAL
 #define SKMP_X2_BAL 1
 #endif
-#ifndef SKMP_X2_ROWSCALAR
-#define SKMP_X2_ROWSCALAR 1
-#endif
+
 #if SKMP_X2_BAL
 struct ColMax {
   f2 v[DG];  // {B, A}
