@@ -1,5 +1,5 @@
 set -x
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build rc=$?
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo BUILD FAILED; tail -20 gpurun_out/build.log; exit 1; }
 for r in 1 2; do for v in rs0 cur; do
   if [ "$v" = cur ]; then L=""; else L=$PWD/paper_2311_03393_b200/libsketchmp_$v.so; fi
   SKMP_LIB=$L python tools/join_bench.py | sed "s/^/$v /"
