@@ -51,6 +51,13 @@ constexpr int C = kJoinCx2;       // rows per staged chunk
 constexpr int CPT = C / NT;       // rows / column records each thread stages per chunk
 constexpr int RS = H + 2 * C;     // ring records
 constexpr int RSD = RS / DG;
+// pitch of the swizzled ring rows: RSD + 1 staggers the DG slot rows across the shared-memory
+// banks (with pitch RSD every slot row starts on the same bank, and the staging cp.asyncs of 32
+// consecutive columns -- one per slot row and ring row -- hit one bank group 8-way)
+#ifndef SKMP_X2_PAD
+#define SKMP_X2_PAD 1
+#endif
+constexpr int RSP = RSD + SKMP_X2_PAD;
 static_assert(RS % DG == 0 && C % (2 * DG) == 0 && (C & (C - 1)) == 0 && C % NT == 0, "geometry");
 
 // ---- f32x2 helpers (64-bit register pairs) ----------------------------------------------------
@@ -88,8 +95,8 @@ struct __align__(16) ColRec0 { f2 df, dg; };   // {df_c, df_c+H}, {dg_c, dg_c+H}
 struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 
 struct Smem {
-  ColRec0 col0[RS];   // swizzled [DG][RSD]
-  f2 col1[RS];        // {inv_c, inv_c+H}
+  ColRec0 col0[DG * RSP];   // swizzled [DG][RSP] (RSD used per row)
+  f2 col1[DG * RSP];        // {inv_c, inv_c+H}
 #if SKMP_X2_ROWSCALAR
   float4 rowq[2 * C];  // raw row records {df, dg, inv, 0}; the f32x2 row operands are formed as
                        // broadcasts {x, x}, which the FFMA2 / FMUL2 encode as .F32 scalar operands
@@ -97,8 +104,8 @@ struct Smem {
   RowRec0 row0[2 * C];
   f2 row1[2 * C];     // {inv_i, inv_i}
 #endif
-  float thrA[RS];     // column thresholds of group A columns (record base c)
-  float thrB[RS];     // ... of group B columns (c + H)
+  float thrA[DG * RSP];     // column thresholds of group A columns (record base c)
+  float thrB[DG * RSP];     // ... of group B columns (c + H)
   float rthr[2 * C];
   // next-chunk key high words (orderable rho), staged by cp.async and converted to the float
   // thresholds above when the chunk ends; the next chunk's records go straight into their ring
@@ -109,7 +116,7 @@ struct Smem {
 // ring slot of column record c (0 <= c < 2^31: n_sub < 2^31, so 32-bit arithmetic suffices)
 __device__ __forceinline__ int pos(int64_t c) {
   const uint32_t p = (uint32_t)c % (uint32_t)RS;
-  return (int)((p % DG) * RSD + p / DG);
+  return (int)((p % DG) * RSP + p / DG);
 }
 
 // masking limits of a thread's diagonals relative to dt (3 registers instead of 2 DG)
@@ -270,14 +277,14 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], ColMax&
 #pragma unroll
   for (int u = 0; u < DG; u += 2) {
     // -- row u: its entering column (slot DG-1) takes the register of the column completed at u-1
-    load_col(X[(u + DG - 1) % DG], sm, ((u + DG - 1) % DG) * RSD + (u == 0 ? qt : qt1));
+    load_col(X[(u + DG - 1) % DG], sm, ((u + DG - 1) % DG) * RSP + (u == 0 ? qt : qt1));
     float ka[DG], kb[DG];
     row_keys<MASKED>(u, cov, X, ROW0(rb + u), ROW1(rb + u), ka, kb, (int)ib + u, lim);
     // columns (ib+u)+dt (A) and +H (B) complete after row u
     const float cA0 = max2(CM.A(u % DG), ka[0]);
     const float cB0 = max2(CM.B(u % DG), kb[0]);
     // -- row u+1 --
-    load_col(X[u % DG], sm, (u % DG) * RSD + qt1);
+    load_col(X[u % DG], sm, (u % DG) * RSP + qt1);
     float la[DG], lb[DG];
     row_keys<MASKED>(u + 1, cov, X, ROW0(rb + u + 1), ROW1(rb + u + 1), la, lb,
                      (int)ib + u + 1, lim);
@@ -319,7 +326,7 @@ __device__ __forceinline__ void rotation_x2(f2 (&cov)[DG], Col (&X)[DG], ColMax&
 #endif
     }
     // -- check-then-publish (rare) --
-    const int t0 = (u % DG) * RSD + qt, t1 = ((u + 1) % DG) * RSD + qt;
+    const int t0 = (u % DG) * RSP + qt, t1 = ((u + 1) % DG) * RSP + qt;
     // ">=": exact ties always reach the atomic (keys independent of tile order / band split)
     const bool hit = (rowa >= sm->rthr[rb + u]) | (rowb >= sm->rthr[rb + u + 1]) | (cA0 >= sm->thrA[t0]) |
                      (cA1 >= sm->thrA[t1]) | (cB0 >= sm->thrB[t0]) | (cB1 >= sm->thrB[t1]);
