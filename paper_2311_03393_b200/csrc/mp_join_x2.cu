@@ -91,6 +91,11 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
 #ifndef SKMP_X2_ROWSCALAR
 #define SKMP_X2_ROWSCALAR 1
 #endif
+// next chunk's column records staged raw (two 16-byte cp.asyncs per column pair) and repacked
+// into the pair layout when the chunk ends, instead of six 4-byte cp.asyncs straight into it
+#ifndef SKMP_X2_RAWCOL
+#define SKMP_X2_RAWCOL 1
+#endif
 struct __align__(16) ColRec0 { f2 df, dg; };   // {df_c, df_c+H}, {dg_c, dg_c+H}
 struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 
@@ -111,6 +116,9 @@ struct Smem {
   // thresholds above when the chunk ends; the next chunk's records go straight into their ring
   // slots (free while this chunk runs) in the pair layout, 4 bytes per cp.async
   int32_t rawtA[C], rawtB[C], rawtR[C];
+#if SKMP_X2_RAWCOL
+  float4 rawcA[C], rawcB[C];  // next chunk's column records c and c + H, raw
+#endif
 };
 
 // ring slot of column record c (0 <= c < 2^31: n_sub < 2^31, so 32-bit arithmetic suffices)
@@ -394,6 +402,10 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
                                            int64_t n_sub_c, int e) {
   const uint32_t c = (uint32_t)c64, i = (uint32_t)i64;
   const uint32_t ns = (uint32_t)n_sub, nsc = (uint32_t)n_sub_c;
+#if SKMP_X2_RAWCOL
+  cp_async16(&sm->rawcA[e], qc + c);
+  cp_async16(&sm->rawcB[e], qc + (c + H));
+#else
   const float* a = reinterpret_cast<const float*>(qc + c);
   const float* b = reinterpret_cast<const float*>(qc + (c + H));
   const int ec = pos(c64);
@@ -405,6 +417,7 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
   cp_async4(d0 + 3, b + 1);
   cp_async4(d1 + 0, a + 2);
   cp_async4(d1 + 1, b + 2);
+#endif
   const int er = (int)(i & (2 * C - 1));
 #if SKMP_X2_ROWSCALAR
   cp_async16(&sm->rowq[er], q + i);  // the raw record, one 16-byte copy
@@ -426,6 +439,16 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
 }
 __device__ __forceinline__ void land_next(Smem* sm, int64_t c, int64_t i, int e) {
   const int ec = pos(c);
+#if SKMP_X2_RAWCOL
+  {
+    const float4 ra = sm->rawcA[e], rb = sm->rawcB[e];
+    ColRec0 r;
+    r.df = pk(ra.x, rb.x);
+    r.dg = pk(ra.y, rb.y);
+    sm->col0[ec] = r;
+    sm->col1[ec] = pk(ra.z, rb.z);
+  }
+#endif
   sm->thrA[ec] = unord32(sm->rawtA[e]);
   sm->thrB[ec] = unord32(sm->rawtB[e]);
   sm->rthr[(int)(i & (2 * C - 1))] = unord32(sm->rawtR[e]);
