@@ -194,6 +194,125 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
   }
 }
 
+// FP64 per-cell threshold tests (SKMP_F64_CELLTEST): an FP64 maximum costs a DSETP and two
+// FSELs (no FP64 3-input max), so instead of reducing row and column maxima in the loop every
+// cell is tested against its row's and its column's threshold with predicate-accumulating DSETPs
+// (row thresholds ride in the row records' 4th word, column thresholds in the unused 4th word of
+// the FP64 ring records, i.e. every threshold arrives with a load the loop already does).  A cell
+// beats its row threshold iff the row maximum does, so the rare publish path reduces the row
+// maxima from the cells still in registers; a column publishes each of its cells that beats the
+// threshold as it is computed (the column's D-cell set has one base, so the set's maximum is
+// published whatever order its cells pass in): the keys are the ones the maxima give, bit for bit.
+#ifndef SKMP_F64_CELLTEST
+#define SKMP_F64_CELLTEST 1
+#endif
+
+template <int D, int RSD_CT>
+__device__ __forceinline__ void publish_ct(int64_t* keys, int64_t* keysc, dq4* rowq, double2* h1, int rbu, int u, int qt,
+                              int qt1, int64_t i_u, int64_t dt, const double (&ka)[D], const double (&kb)[D],
+                              dq4 (&X)[D]) {
+  const double rowa = tree_max<double, D>(ka), rowb = tree_max<double, D>(kb);
+  if (rowa >= rowq[rbu].w) {
+    publish(keys, i_u, rowa, i_u + dt);
+    rowq[rbu].w = rowa;
+  }
+  if (rowb >= rowq[rbu + 1].w) {
+    publish(keys, i_u + 1, rowb, i_u + 1 + dt);
+    rowq[rbu + 1].w = rowb;
+  }
+  // cells (i_u + v, c = i_u + v + dt + d), c - (ib + dt) = s = u + v + d: a column gets its
+  // row pair's cells merged (one publish); ring slot s RSD + qt (s < D) or (s - D) RSD + qt1; the
+  // column's rows in this thread start at c - dt - D + 1 = i_u - u + s - D + 1
+#pragma unroll
+  for (int s = u; s <= u + D; ++s) {
+    const double x = s == u ? ka[0] : (s == u + D ? kb[D - 1] : max2(ka[s - u], kb[s - u - 1]));
+    const int p = s < D ? s * RSD_CT + qt : (s - D) * RSD_CT + qt1;
+    if (x >= h1[p].y) {
+      publish(keysc, i_u - u + s + dt, x, i_u - u + s - (D - 1));
+      h1[p].y = x;
+    }
+  }
+  // the columns still in registers (s = u+1 .. u+D) take their current thresholds: a stale copy
+  // would send the warp down this path again for cells that cannot improve the key
+#pragma unroll
+  for (int s = u + 1; s <= u + D; ++s) X[s % D].w = h1[s < D ? s * RSD_CT + qt : (s - D) * RSD_CT + qt1].y;
+}
+
+// hit |= (k >= t) for 16 (k, t) pairs with predicate-accumulating setp (written out in PTX:
+// from C++ the compiler fuses (k >= a) | (k >= b) into k >= min(a, b), a DSETP.MIN plus
+// NaN-fixing selects per cell)
+__device__ __forceinline__ bool any_ge(const double (&k)[16], const double (&t)[16]) {
+  unsigned r;
+  asm("{ .reg .pred p;\n"
+      "  setp.ge.f64 p, %1, %17;\n"
+      "  setp.ge.or.f64 p, %2, %18, p;\n"
+      "  setp.ge.or.f64 p, %3, %19, p;\n"
+      "  setp.ge.or.f64 p, %4, %20, p;\n"
+      "  setp.ge.or.f64 p, %5, %21, p;\n"
+      "  setp.ge.or.f64 p, %6, %22, p;\n"
+      "  setp.ge.or.f64 p, %7, %23, p;\n"
+      "  setp.ge.or.f64 p, %8, %24, p;\n"
+      "  setp.ge.or.f64 p, %9, %25, p;\n"
+      "  setp.ge.or.f64 p, %10, %26, p;\n"
+      "  setp.ge.or.f64 p, %11, %27, p;\n"
+      "  setp.ge.or.f64 p, %12, %28, p;\n"
+      "  setp.ge.or.f64 p, %13, %29, p;\n"
+      "  setp.ge.or.f64 p, %14, %30, p;\n"
+      "  setp.ge.or.f64 p, %15, %31, p;\n"
+      "  setp.ge.or.f64 p, %16, %32, p;\n"
+      "  selp.u32 %0, 1, 0, p; }"
+      : "=r"(r)
+      : "d"(k[0]), "d"(k[1]), "d"(k[2]), "d"(k[3]), "d"(k[4]), "d"(k[5]), "d"(k[6]), "d"(k[7]), "d"(k[8]),
+        "d"(k[9]), "d"(k[10]), "d"(k[11]), "d"(k[12]), "d"(k[13]), "d"(k[14]), "d"(k[15]), "d"(t[0]), "d"(t[1]),
+        "d"(t[2]), "d"(t[3]), "d"(t[4]), "d"(t[5]), "d"(t[6]), "d"(t[7]), "d"(t[8]), "d"(t[9]), "d"(t[10]),
+        "d"(t[11]), "d"(t[12]), "d"(t[13]), "d"(t[14]), "d"(t[15]));
+  return r != 0;
+}
+
+template <int D, int RSD, bool MASKED>
+__device__ __forceinline__ void rotation_ct(double (&cov)[D], dq4 (&X)[D], const dq4* rowp, RingView<double> rv,
+                                            int p0, int p1, dq4* rowq, int rb, int qt, int64_t ib, int64_t dt,
+                                            const int (&lim)[D], int64_t* keys, int64_t* keysc) {
+#pragma unroll
+  for (int u = 0; u < D; u += 2) {
+    // -- row u --
+    const dq4 ra = rowp[u];
+    X[(u + D - 1) % D] = rv.load(((u + D - 1) % D) * RSD + (u == 0 ? p0 : p1));
+    double ka[D], kk[4 * D], tt[4 * D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const dq4& x = X[(u + d) % D];
+      cov[d] = fma(ra.x, x.y, cov[d]);
+      cov[d] = fma(x.x, ra.y, cov[d]);
+      ka[d] = (cov[d] * x.z) * ra.z;
+      if (MASKED) ka[d] = ((int)ib + u < lim[d]) ? ka[d] : neg_inf<double>();
+      kk[2 * d] = ka[d];
+      tt[2 * d] = ra.w;
+      kk[2 * d + 1] = ka[d];
+      tt[2 * d + 1] = x.w;
+    }
+    // -- row u+1 (its entering column reuses the register of row u's completed column) --
+    const dq4 rbq = rowp[u + 1];
+    X[u % D] = rv.load((u % D) * RSD + p1);
+    double kb[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const dq4& x = X[(u + 1 + d) % D];
+      cov[d] = fma(rbq.x, x.y, cov[d]);
+      cov[d] = fma(x.x, rbq.y, cov[d]);
+      kb[d] = (cov[d] * x.z) * rbq.z;
+      if (MASKED) kb[d] = ((int)ib + u + 1 < lim[d]) ? kb[d] : neg_inf<double>();
+      kk[2 * D + 2 * d] = kb[d];
+      tt[2 * D + 2 * d] = rbq.w;
+      kk[2 * D + 2 * d + 1] = kb[d];
+      tt[2 * D + 2 * d + 1] = x.w;
+    }
+    // ">=": exact ties reach the atomic (keys independent of tile order / band split)
+    if (__any_sync(0xffffffffu, any_ge(kk, tt)))
+      publish_ct<D, RSD>(keys, keysc, rowq, rv.h1, rb + u, u, qt, (qt + 1 == RSD) ? 0 : qt + 1, ib + u, dt, ka, kb, X);
+  }
+}
+
 template <typename T, int D, int NT, int C, bool MASKED>
 __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delta0, int64_t i0,
                                           int64_t i1, unsigned char* smem_raw) {
@@ -207,6 +326,11 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   Q* rowq = ring + RS;
   T* cthr = reinterpret_cast<T*>(rowq + 2 * C);
 
+  // FP64 per-cell tests: column thresholds live in the ring records' 4th word (h1[p].y)
+  constexpr bool CT = (sizeof(T) == 8) && SKMP_F64_CELLTEST;
+  auto col_thr = [&](int p) -> T& {
+    if constexpr (CT) return rv.h1[p].y; else return cthr[p];
+  };
   const int tid = threadIdx.x;
   const int64_t n_sub = a.n_sub, n_sub_c = a.n_sub_c;  // rows: i < n_sub; columns: j < n_sub_c
   constexpr int words = sizeof(T) == 4 ? 1 : 2;
@@ -273,14 +397,21 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   for (int e = tid; e < W + C; e += NT) {
     const int64_t c = i0 + delta0 + e;
     rv.stage(G::pos(c), &qc[c]);
-    cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
+    if constexpr (!CT) cthr[G::pos(c)] = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
   }
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
     stage_q<T>(&rowq[i % (2 * C)], &q[i]);
   }
   cp_async_wait_all();
-  // row thresholds go into the staged row records' 4th word once the copies have landed
+  // row thresholds go into the staged row records' 4th word once the copies have landed (and,
+  // with CT, the column thresholds into the ring records')
+  if constexpr (CT) {
+    for (int e = tid; e < W + C; e += NT) {
+      const int64_t c = i0 + delta0 + e;
+      col_thr(G::pos(c)) = (c < n_sub_c) ? load_thr(keysc, c, (T*)nullptr) : pos_inf<T>();
+    }
+  }
   for (int e = tid; e < C; e += NT) {
     const int64_t i = i0 + e;
     rowq[i % (2 * C)].w = (i < n_sub) ? load_thr(keys, i, (T*)nullptr) : pos_inf<T>();
@@ -328,12 +459,19 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     const bool cmasked = MASKED && (diag_masked || (rend - 1) + delta0 + W - 1 >= n_sub_c || rend > n_sub);
     for (int it = 0; it < nrot; ++it, ib += D) {
       const int qt1 = (qt + 1 == RSD) ? 0 : qt + 1;
-      if (cmasked)
-        rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
-                                  rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
-      else
-        rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
-                                   rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
+      if constexpr (CT) {
+        if (cmasked)
+          rotation_ct<D, RSD, true>(cov, X, rowq + rb, rv, qt, qt1, rowq, rb, qt, ib, dt, lim, keys, keysc);
+        else
+          rotation_ct<D, RSD, false>(cov, X, rowq + rb, rv, qt, qt1, rowq, rb, qt, ib, dt, lim, keys, keysc);
+      } else {
+        if (cmasked)
+          rotation<T, D, RSD, true>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
+                                    rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
+        else
+          rotation<T, D, RSD, false>(cov, X, CK, rowq + rb, rv, qt, qt1, cthr + qt,
+                                     rowq, cthr, rb, qt, ib, dt, lim, keys, keysc);
+      }
       qt = qt1;
       rb = (rb + D) & (2 * C - 1);
     }
@@ -343,7 +481,7 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
     if (more) {
 #pragma unroll
       for (int e = 0; e < CPT; ++e) {
-        cthr[G::pos(r + delta0 + W + C + tid + e * NT)] = nthr_c[e];
+        col_thr(G::pos(r + delta0 + W + C + tid + e * NT)) = nthr_c[e];
         rowq[(r + C + tid + e * NT) % (2 * C)].w = nthr_r[e];
       }
     }
@@ -353,8 +491,9 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
   // ---- epilogue: the D-1 columns still open after the last row hold partial maxima ----------
   // After row i1-1 the open columns are (i1 - 1) + dt + d for d = 1..D-1, i.e. register
   // x = d - 1 holds column i1 + dt + x.
+  // (CT: every cell was tested and published as it was computed: nothing is open)
 #pragma unroll
-  for (int x = 0; x < D - 1; ++x) {
+  for (int x = 0; x < (CT ? 0 : D - 1); ++x) {
     const T v = CK[x];
     const int64_t c = i1 + dt + x;
     if (c < n_sub_c && v >= cthr[G::pos(c)]) publish(keysc, c, v, c - dt - (D - 1));
@@ -364,8 +503,11 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #ifndef SKMP_JOIN_MINB
 #define SKMP_JOIN_MINB 20  // FP32 D=8: cap at ~96 registers -> 20 warps/SM (measured best)
 #endif
+#ifndef SKMP_JOIN_MINB64
+#define SKMP_JOIN_MINB64 1
+#endif
 template <typename T, int D, int NT, int C>
-__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : 1))
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : SKMP_JOIN_MINB64))
 join_kernel(JoinArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = NT * D;

@@ -103,7 +103,7 @@ if __name__ == "__main__":
     need = int(sys.argv[3]) if len(sys.argv) > 3 else 8
     for b in blocks(sass(path, pat)):
         c = collections.Counter(parse(x)[0].split(".")[0] for _, x in b)
-        nfp = c["FFMA2"] + c["FMUL2"] + c["FFMA"] + c["FMUL"]
+        nfp = c["FFMA2"] + c["FMUL2"] + c["FFMA"] + c["FMUL"] + c["DFMA"] + c["DMUL"]
         if nfp < need:
             continue
         rf, fma, alu, issue = model(b)
