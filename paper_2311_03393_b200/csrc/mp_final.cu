@@ -52,11 +52,11 @@ __device__ __forceinline__ int64_t smallest_adm_flat(const int32_t* F, int32_t n
 
 // Transposed warp sum of N per-lane values: afterwards every lane holds in v[0] the warp total
 // of value xidx<N>(lane) (log2(N) exchange steps keep half the values each, then plain steps).
-template <int N>
+template <int N, int L = 32>
 __device__ __forceinline__ void xsum(double (&v)[N], int lane) {
   int c = N;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
+  for (int o = L / 2; o >= 1; o >>= 1) {
     if (c > 1) {
       const bool up = (lane & o) != 0;
 #pragma unroll
@@ -73,11 +73,11 @@ __device__ __forceinline__ void xsum(double (&v)[N], int lane) {
     }
   }
 }
-template <int N>
+template <int N, int L = 32>
 __device__ __forceinline__ int xidx(int lane) {
   int idx = 0, c = N;
 #pragma unroll
-  for (int o = 16; o >= 1 && c > 1; o >>= 1) {
+  for (int o = L / 2; o >= 1 && c > 1; o >>= 1) {
     c >>= 1;
     if (lane & o) idx += c;
   }
@@ -353,11 +353,11 @@ __device__ __forceinline__ void reg_stage(T* buf, const T* R, const T* Ro, int64
 }
 
 // the lane holding candidate d after xsum<N> (inverse of xidx<N>)
-template <int N>
+template <int N, int L = 32>
 __device__ __forceinline__ int xlane(int d) {
   int lane = 0, c = N;
 #pragma unroll
-  for (int o = 16; o >= 1 && c > 1; o >>= 1) {
+  for (int o = L / 2; o >= 1 && c > 1; o >>= 1) {
     c >>= 1;
     if (d & c) lane |= o;
   }
@@ -371,14 +371,14 @@ struct FinPre {
   double mi, ii, mc, ic;
   bool fi, fc;
 };
-template <int SPAN>
+template <int SPAN, int L = 32>
 __device__ __forceinline__ FinPre fin_pre(const MpDev& w, const MpDev& wo, int64_t o, int64_t oo, int64_t i,
                                           int64_t b, int lane) {
   FinPre p;
   p.mi = w.mu[o + i];
   p.ii = w.isig64[o + i];
   p.fi = w.flat[o + i] != 0;
-  int64_t jc = b + xidx<SPAN>(lane);
+  int64_t jc = b + xidx<SPAN, L>(lane);
   jc = jc < 0 ? 0 : (jc >= wo.n_sub ? wo.n_sub - 1 : jc);
   p.mc = wo.mu[oo + jc];
   p.ic = wo.isig64[oo + jc];
@@ -544,10 +544,259 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
   }
 }
 
+// ---- half-warp variant: 16 lanes per row, two rows per warp -----------------------------------
+// The register kernel above spends ~590 warp instructions per row of which only 64 are the
+// DFMAs of the SPAN dot products: the rest is per-row scalar work (key decode, statistics,
+// staging addresses, the reductions, the argmin, flat handling, the store) that every lane of
+// the warp executes for the one row.  Here each half-warp owns a row (lane l of the half holds the
+// E = m/16 consecutive positions [E l, E l + E)), so every such instruction serves two rows; the
+// DFMA count per row is unchanged (twice the positions per lane) and the reductions need one
+// butterfly round fewer.  Per-half buffers are padded to (E+1)-element groups like the register
+// kernel's and the two halves sit 16 (mod 32) elements apart: lane l of a half reads bank
+// ((E+1) l + e) mod 32, the other half the 16 complementary banks, so a warp's shared loads stay
+// conflict-free.  Shuffles never cross the halves (xor offsets < 16, sources within the half);
+// the rare explicit-difference pass is entered by the whole warp when either half needs it.
+template <int E, int SPAN> struct HwBuf {
+  static constexpr int NI = 16 * E;               // row window positions (>= m)
+  static constexpr int NO = 16 * E + SPAN - 1;    // candidate positions (>= m + SPAN - 1)
+  static constexpr int XI = pad_pos<E>(NI - 1) + 1;
+  static constexpr int XO = pad_pos<E>(NO - 1) + 1;
+  static constexpr int HS = ((XI + XO + 15) / 32) * 32 + 16;  // half stride, = 16 (mod 32)
+};
+
+// stage row i's window and the candidate windows of base b into one half's buffer (lane l of the
+// half: positions l + 16 q, padded to l + l/E + q (16 + 16/E); tails stay zero, see reg_stage)
+template <typename T, int E, int SPAN, bool FULL>
+__device__ __forceinline__ void hw_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int m,
+                                         int64_t n_o, int l) {
+  using B = HwBuf<E, SPAN>;
+  static_assert(16 % E == 0 || E == 16, "E must divide 16");
+  T* xi = buf + l + l / E;
+  T* xo = buf + B::XI + l + l / E;
+  constexpr int QS = 16 + 16 / E;
+  const T* gi = R + i + l;
+#pragma unroll
+  for (int q = 0; q < E; ++q)
+    if (FULL || l + 16 * q < m) cp_async_b(xi + q * QS, gi + 16 * q, (int)sizeof(T));
+  const int no_used = FULL ? 16 * E + SPAN - 1 : m + SPAN - 1;  // (FULL: m = 16 E, compile-time masks)
+  if (b >= 0 && b + no_used <= n_o) {
+    const T* go = Ro + b + l;
+#pragma unroll
+    for (int q = 0; q < (B::NO + 15) / 16; ++q)
+      if (l + 16 * q < no_used) cp_async_b(xo + q * QS, go + 16 * q, (int)sizeof(T));
+  } else {
+    const int32_t ob = (int32_t)b, no = (int32_t)n_o;
+#pragma unroll
+    for (int q = 0; q < (B::NO + 15) / 16; ++q) {
+      const int t = l + 16 * q;
+      if (t < no_used) {
+        int32_t idx = ob + t;
+        idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);
+        cp_async_b(xo + q * QS, Ro + idx, (int)sizeof(T));
+      }
+    }
+  }
+}
+
+#ifndef SKMP_FIN_HW_MINB
+#define SKMP_FIN_HW_MINB 4  // 128 registers: 16 warps (32 rows in flight) per SM
+#endif
+// fin_pre with 32-bit window indices from per-series base pointers (n_sub < 2^31)
+struct FinBase {
+  const double *mu, *isig;
+  const unsigned char* flat;
+};
+template <int SPAN>
+__device__ __forceinline__ FinPre fin_pre32(const FinBase& r, const FinBase& c, int32_t i, int32_t b, int32_t nso,
+                                            int l) {
+  FinPre p;
+  p.mi = r.mu[i];
+  p.ii = r.isig[i];
+  p.fi = r.flat[i] != 0;
+  int32_t jc = b + xidx<SPAN, 16>(l);
+  jc = jc < 0 ? 0 : (jc >= nso ? nso - 1 : jc);
+  p.mc = c.mu[jc];
+  p.ic = c.isig[jc];
+  p.fc = c.flat[jc] != 0;
+  return p;
+}
+
+template <typename T, int SPAN, int E, bool FULL>
+__global__ void __launch_bounds__(32 * kFinRegWarps, SKMP_FIN_HW_MINB)
+finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
+                   int64_t* __restrict__ I) {
+  static_assert(SPAN <= 16 && (SPAN & (SPAN - 1)) == 0, "geometry");
+  using B = HwBuf<E, SPAN>;
+  __shared__ __align__(16) T fsm[kFinRegWarps * 4 * B::HS];
+  const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15;
+  T* hb = fsm + (threadIdx.x >> 5) * 4 * B::HS + h * B::HS;  // this half's buffer 0; buffer 1 at + 2 HS
+  const int64_t i_first = row_lo + ((int64_t)blockIdx.x * kFinRegWarps + (threadIdx.x >> 5)) * (2 * kFinRows);
+  const int g = blockIdx.y;
+  const int words = (w.dtype == SKMP_F32) ? 1 : 2;
+  const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
+  const int64_t o = (int64_t)g * w.ldq, oo = (int64_t)g * wo.ldq;
+  const T* R = static_cast<const T*>(w.R) + (int64_t)g * w.ld;
+  const T* Ro = static_cast<const T*>(wo.R) + (int64_t)g * wo.ld;
+  const int m = w.m;
+  const double sqm = sqrt((double)m);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll), nan = __longlong_as_double(0x7ff8000000000000ll);
+  const int32_t nf = wo.nflat[g];
+  const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
+  // half h walks rows i_first + 2 rr + h
+  auto row_of = [&](int rr) { const int64_t x = i_first + 2 * rr + h; return x < row_hi ? x : row_hi - 1; };
+  auto base_of = [&](int64_t kw) { int64_t kb = 0; return key_arg(kw, words, &kb) ? kb : (int64_t)0; };
+  int64_t kw_cur = key_word(keys, row_of(0), words);
+  int64_t kw_nxt = key_word(keys, row_of(1), words);
+  {
+    T* wb = fsm + (threadIdx.x >> 5) * 4 * B::HS;
+    for (int q = lane; q < 4 * B::HS; q += 32) wb[q] = (T)0;  // tails stay zero
+  }
+  __syncwarp();
+  const FinBase rbase{w.mu + o, w.isig64 + o, w.flat + o}, cbase{wo.mu + oo, wo.isig64 + oo, wo.flat + oo};
+  const int32_t nso = (int32_t)wo.n_sub;
+  // clamping b to [-32, n_sub] first keeps clamp(b + x, 0, n_sub - 1) for x < 16 (32-bit safe)
+  auto b32 = [nso](int64_t b) { return (int32_t)(b < -32 ? -32 : (b > nso ? (int64_t)nso : b)); };
+  hw_stage<T, E, SPAN, FULL>(hb, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, l);
+  cp_async_commit();
+  FinPre pre = fin_pre32<SPAN>(rbase, cbase, (int32_t)row_of(0), b32(base_of(kw_cur)), nso, l);
+  for (int rr = 0; rr < kFinRows; ++rr) {
+    const int64_t i_raw = i_first + 2 * rr + h;
+    const bool live = i_raw < row_hi;
+    const int64_t i = row_of(rr);
+    const int64_t kw = kw_cur;
+    const FinPre cu = pre;
+    T* cur = hb + (rr & 1) * 2 * B::HS;
+    if (rr + 1 < kFinRows) {
+      const int64_t bn = base_of(kw_nxt);
+      hw_stage<T, E, SPAN, FULL>(hb + ((rr + 1) & 1) * 2 * B::HS, R, Ro, row_of(rr + 1), bn, m, wo.n, l);
+      pre = fin_pre32<SPAN>(rbase, cbase, (int32_t)row_of(rr + 1), b32(bn), nso, l);
+    }
+    cp_async_commit();
+    kw_cur = kw_nxt;
+    kw_nxt = key_word(keys, row_of(rr + 2 < kFinRows ? rr + 2 : kFinRows - 1), words);
+    cp_async_wait1();
+    __syncwarp();
+    int64_t kb = 0;
+    const bool has = key_arg(kw, words, &kb);
+    const int64_t b = has ? kb : 0;
+    const double mi = cu.mi;
+    // ---- the SPAN candidate dot products over this lane's E positions -----------------------
+    const T* xi = cur + (E + 1) * l;           // position E l + e at (E+1) l + e
+    const T* xo = cur + B::XI + (E + 1) * l;   // position E l + t at (E+1) l + t + t / E
+    double acc[SPAN], asum = 0.0;
+#pragma unroll
+    for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
+    double a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int s = E * l + e;
+      a[e] = (FULL || s < m) ? (double)xi[e] - mi : 0.0;
+      asum += a[e];
+    }
+#pragma unroll
+    for (int t = 0; t < E + SPAN - 1; ++t) {
+      const double wt = (double)xo[t + t / E];
+#pragma unroll
+      for (int d = 0; d < SPAN; ++d) {
+        const int e = t - d;
+        if (e >= 0 && e < E) acc[d] = fma(a[e], wt, acc[d]);
+      }
+    }
+#pragma unroll
+    for (int q = 8; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+    xsum<SPAN, 16>(acc, l);
+    int d = xidx<SPAN, 16>(l);
+    double dd = inf;
+    const int64_t jd = b + d;
+    if (admissible(i, jd, wo.n_sub, excl)) {
+      if (cu.fc) {
+        dd = (double)m;
+      } else {
+        const double cov = acc[0] - cu.mc * asum;
+        dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
+      }
+    }
+    // argmin over the SPAN candidates (16 / SPAN lanes of a half hold each)
+#pragma unroll
+    for (int q = 8; q >= 16 / SPAN; q >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, dd, q);
+      const int oi = __shfl_xor_sync(0xffffffffu, d, q);
+      if (od < dd || (od == dd && oi < d)) {
+        dd = od;
+        d = oi;
+      }
+    }
+    const int64_t jr = dd < inf ? b + d : -1;
+    const int src = (lane & 16) | xlane<SPAN, 16>(jr >= 0 ? d : 0);
+    const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
+    const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
+    const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
+    const bool exact = jr >= 0 && !fj;
+    const int de = exact ? d : 0;
+    double pe = sqrt(dd > 0.0 ? dd : 0.0);
+    const bool need = exact && dd < kFinExplicitBelow;
+    if (__any_sync(0xffffffffu, need)) {  // whole warp (the reduction shuffles span both halves)
+      const double ii = cu.ii;
+      double acc2 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int s = E * l + e;
+        const double zi = __dmul_rn(a[e], ii);
+        const double zj = __dmul_rn((double)cur[B::XI + pad_pos<E>(s + de)] - mj, ij);
+        const double df = zi - zj;
+        acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
+      }
+#pragma unroll
+      for (int q = 8; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+      if (need) pe = sqrt(acc2);
+    }
+    double p;
+    int64_t j;
+    if (cu.fi) {
+      const int64_t f = smallest_adm_flat(F, nf, i, excl);
+      if (f >= 0) {
+        p = 0.0;
+        j = f;
+      } else {
+        p = sqm;
+        j = (excl < 0 || i - excl - 1 >= 0) ? 0 : i + excl + 1;
+      }
+    } else if (!has) {
+      p = nan;
+      j = -1;
+    } else {
+      j = jr;
+      p = jr < 0 ? nan : (exact ? pe : sqm);
+      if (nf > 0) {
+        const int64_t f = smallest_adm_flat(F, nf, i, excl);
+        if (f >= 0 && (sqm < p || (sqm == p && f < j) || j < 0)) {
+          p = sqm;
+          j = f;
+        }
+      }
+    }
+    if (l == 0 && live) {
+      P[(int64_t)g * w.n_sub + i] = (T)p;
+      I[(int64_t)g * w.n_sub + i] = j;
+    }
+    __syncwarp();  // this buffer is refilled two rows later
+  }
+}
+
 bool fin_reg_enabled() {
   static const bool on = [] {
     const char* e = getenv("SKMP_FIN_IMPL");  // "smem": the shared-memory variant (A/B)
     return !(e && e[0] == 's');
+  }();
+  return on;
+}
+#ifndef SKMP_FIN_HW
+#define SKMP_FIN_HW 1
+#endif
+bool fin_hw_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SKMP_FIN_IMPL");  // "reg": the full-warp register kernel (A/B)
+    return SKMP_FIN_HW && !(e && (e[0] == 'r' || e[0] == 's'));
   }();
   return on;
 }
@@ -563,6 +812,33 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
   const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
 #define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
+  // (FP64 windows longer than 128 keep the full-warp kernel: 16-position FP64 buffers exceed the
+  // static shared-memory limit)
+  if ((f32 ? w.m <= 256 : w.m <= 128) && (w.span == 4 || w.span == 8) && fin_hw_enabled()) {
+    const int Eh = w.m <= 64 ? 4 : (w.m <= 128 ? 8 : 16);
+    const int64_t perh = (int64_t)kFinRegWarps * 2 * kFinRows;
+    grid.x = (unsigned)((row_hi - row_lo + perh - 1) / perh);
+    const int nth = 32 * kFinRegWarps;
+#define SKMP_FINH(TT, SP, EE)                                                                                   \
+  do {                                                                                                          \
+    if (w.m == 16 * (EE))                                                                                       \
+      finalize_hw_kernel<TT, SP, EE, true><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+    else                                                                                                        \
+      finalize_hw_kernel<TT, SP, EE, false><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+  } while (0)
+    if (w.span == 8) {
+      if (Eh == 4) { if (f32) SKMP_FINH(float, 8, 4); else SKMP_FINH(double, 8, 4); }
+      else if (Eh == 8) { if (f32) SKMP_FINH(float, 8, 8); else SKMP_FINH(double, 8, 8); }
+      else SKMP_FINH(float, 8, 16);
+    } else {
+      if (Eh == 4) { if (f32) SKMP_FINH(float, 4, 4); else SKMP_FINH(double, 4, 4); }
+      else if (Eh == 8) { if (f32) SKMP_FINH(float, 4, 8); else SKMP_FINH(double, 4, 8); }
+      else SKMP_FINH(float, 4, 16);
+    }
+#undef SKMP_FINH
+    count_launches(1);
+    return cudaGetLastError();
+  }
   const int E = w.m <= 64 ? 2 : (w.m <= 128 ? 4 : (w.m <= 256 ? 8 : 0));
   if (E > 0 && (w.span == 4 || w.span == 8) && fin_reg_enabled()) {
     const int64_t perr = (int64_t)kFinRegWarps * kFinRows;
