@@ -544,76 +544,81 @@ finalize_reg_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi,
   }
 }
 
-// ---- half-warp variant: 16 lanes per row, two rows per warp -----------------------------------
+// ---- sub-warp variant: LPR = 16 or 8 lanes per row, 32 / LPR rows per warp ---------------------
 // The register kernel above spends ~590 warp instructions per row of which only 64 are the
 // DFMAs of the SPAN dot products: the rest is per-row scalar work (key decode, statistics,
 // staging addresses, the reductions, the argmin, flat handling, the store) that every lane of
-// the warp executes for the one row.  Here each half-warp owns a row (lane l of the half holds the
-// E = m/16 consecutive positions [E l, E l + E)), so every such instruction serves two rows; the
-// DFMA count per row is unchanged (twice the positions per lane) and the reductions need one
-// butterfly round fewer.  Per-half buffers are padded to (E+1)-element groups like the register
-// kernel's and the two halves sit 16 (mod 32) elements apart: lane l of a half reads bank
-// ((E+1) l + e) mod 32, the other half the 16 complementary banks, so a warp's shared loads stay
-// conflict-free.  Shuffles never cross the halves (xor offsets < 16, sources within the half);
-// the rare explicit-difference pass is entered by the whole warp when either half needs it.
-template <int E, int SPAN> struct HwBuf {
-  static constexpr int NI = 16 * E;               // row window positions (>= m)
-  static constexpr int NO = 16 * E + SPAN - 1;    // candidate positions (>= m + SPAN - 1)
-  static constexpr int XI = pad_pos<E>(NI - 1) + 1;
-  static constexpr int XO = pad_pos<E>(NO - 1) + 1;
-  static constexpr int HS = ((XI + XO + 15) / 32) * 32 + 16;  // half stride, = 16 (mod 32)
+// the warp executes for the one row.  Here a group of LPR lanes owns a row (lane l of the group
+// holds the E = m / LPR consecutive positions [E l, E l + E)), so every such instruction serves
+// 32 / LPR rows; the DFMA count per row is unchanged and the reductions need fewer butterfly
+// rounds.  Each lane's E positions sit contiguously in its group's buffer, the lanes' runs 16
+// bytes apart (padded position s + PAD (s / E), PAD = 16 / sizeof(T)), so the row and candidate
+// values are read with 128-bit shared loads at a 16-byte-aligned stride of E + PAD elements:
+// the 8 lanes of a quarter-warp phase hit 8 distinct 4-bank groups (conflict-free).  Shuffles
+// never leave a group (xor offsets < LPR, sources inside the group); the rare explicit-
+// difference pass is entered by the whole warp when any group needs it.
+template <typename T, int E, int LPR, int SPAN> struct HwBuf {
+  static constexpr int PAD = 16 / (int)sizeof(T);
+  static constexpr int VEC = 16 / (int)sizeof(T);                 // elements per 128-bit load
+  static constexpr int NI = LPR * E;                              // row window positions (>= m)
+  static constexpr int NO = LPR * E + SPAN - 1;                   // candidate positions
+  static constexpr int padded(int s) { return s + PAD * (s / E); }
+  static constexpr int up(int x) { return (x + PAD - 1) / PAD * PAD; }
+  static constexpr int XI = up(padded(NI - 1) + 1);
+  static constexpr int XO = up(padded(NO - 1) + 1 + VEC);         // + VEC: the last vector may overrun
+  static constexpr int HS = XI + XO;                              // elements per row buffer
+  static constexpr int NW = (E + SPAN - 1 + VEC - 1) / VEC;       // candidate vectors per lane
 };
+template <int LPR> struct HwCta { static constexpr int W = LPR == 8 ? 2 : 4; };  // warps per CTA
 
-// stage row i's window and the candidate windows of base b into one half's buffer (lane l of the
-// half: positions l + 16 q, padded to l + l/E + q (16 + 16/E); tails stay zero, see reg_stage)
-template <typename T, int E, int SPAN, bool FULL>
+// stage row i's window and the candidate windows of base b into one group's buffer: lane l of
+// the group copies positions l + LPR q (padded: l + PAD (l / E) + LPR q + PAD ((LPR q) / E), a
+// lane base plus compile-time offsets); tails stay zero from the kernel start (see reg_stage)
+template <typename T, int E, int LPR, int SPAN, bool FULL>
 __device__ __forceinline__ void hw_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int m,
                                          int64_t n_o, int l) {
-  using B = HwBuf<E, SPAN>;
-  static_assert(16 % E == 0 || E == 16, "E must divide 16");
-  T* xi = buf + l + l / E;
-  T* xo = buf + B::XI + l + l / E;
-  constexpr int QS = 16 + 16 / E;
+  using B = HwBuf<T, E, LPR, SPAN>;
+  static_assert(E % LPR == 0 || LPR % E == 0, "E and LPR must divide one another");
+  T* xi = buf + l + B::PAD * (l / E);
+  T* xo = buf + B::XI + l + B::PAD * (l / E);
   const T* gi = R + i + l;
 #pragma unroll
   for (int q = 0; q < E; ++q)
-    if (FULL || l + 16 * q < m) cp_async_b(xi + q * QS, gi + 16 * q, (int)sizeof(T));
-  const int no_used = FULL ? 16 * E + SPAN - 1 : m + SPAN - 1;  // (FULL: m = 16 E, compile-time masks)
+    if (FULL || l + LPR * q < m) cp_async_b(xi + LPR * q + B::PAD * ((LPR * q) / E), gi + LPR * q, (int)sizeof(T));
+  const int no_used = FULL ? LPR * E + SPAN - 1 : m + SPAN - 1;  // (FULL: m = LPR E, compile-time masks)
+  constexpr int NQ = (B::NO + LPR - 1) / LPR;
   if (b >= 0 && b + no_used <= n_o) {
     const T* go = Ro + b + l;
 #pragma unroll
-    for (int q = 0; q < (B::NO + 15) / 16; ++q)
-      if (l + 16 * q < no_used) cp_async_b(xo + q * QS, go + 16 * q, (int)sizeof(T));
+    for (int q = 0; q < NQ; ++q)
+      if (l + LPR * q < no_used) cp_async_b(xo + LPR * q + B::PAD * ((LPR * q) / E), go + LPR * q, (int)sizeof(T));
   } else {
     const int32_t ob = (int32_t)b, no = (int32_t)n_o;
 #pragma unroll
-    for (int q = 0; q < (B::NO + 15) / 16; ++q) {
-      const int t = l + 16 * q;
+    for (int q = 0; q < NQ; ++q) {
+      const int t = l + LPR * q;
       if (t < no_used) {
         int32_t idx = ob + t;
         idx = idx < 0 ? 0 : (idx >= no ? no - 1 : idx);
-        cp_async_b(xo + q * QS, Ro + idx, (int)sizeof(T));
+        cp_async_b(xo + LPR * q + B::PAD * ((LPR * q) / E), Ro + idx, (int)sizeof(T));
       }
     }
   }
 }
 
-#ifndef SKMP_FIN_HW_MINB
-#define SKMP_FIN_HW_MINB 4  // 128 registers: 16 warps (32 rows in flight) per SM
-#endif
 // fin_pre with 32-bit window indices from per-series base pointers (n_sub < 2^31)
 struct FinBase {
   const double *mu, *isig;
   const unsigned char* flat;
 };
-template <int SPAN>
+template <int SPAN, int LPR>
 __device__ __forceinline__ FinPre fin_pre32(const FinBase& r, const FinBase& c, int32_t i, int32_t b, int32_t nso,
                                             int l) {
   FinPre p;
   p.mi = r.mu[i];
   p.ii = r.isig[i];
   p.fi = r.flat[i] != 0;
-  int32_t jc = b + xidx<SPAN, 16>(l);
+  int32_t jc = b + xidx<SPAN, LPR>(l);
   jc = jc < 0 ? 0 : (jc >= nso ? nso - 1 : jc);
   p.mc = c.mu[jc];
   p.ic = c.isig[jc];
@@ -621,16 +626,36 @@ __device__ __forceinline__ FinPre fin_pre32(const FinBase& r, const FinBase& c, 
   return p;
 }
 
-template <typename T, int SPAN, int E, bool FULL>
-__global__ void __launch_bounds__(32 * kFinRegWarps, SKMP_FIN_HW_MINB)
+// VEC consecutive staged values as doubles (one 128-bit shared load)
+template <typename T> __device__ __forceinline__ void ld_vec(const T* p, double* o);
+template <> __device__ __forceinline__ void ld_vec<float>(const float* p, double* o) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+  o[3] = v.w;
+}
+template <> __device__ __forceinline__ void ld_vec<double>(const double* p, double* o) {
+  const double2 v = *reinterpret_cast<const double2*>(p);
+  o[0] = v.x;
+  o[1] = v.y;
+}
+
+#ifndef SKMP_FIN_HW_MINB
+#define SKMP_FIN_HW_MINB 4  // (x 128 threads) 128 registers
+#endif
+template <typename T, int SPAN, int E, int LPR, bool FULL>
+__global__ void __launch_bounds__(32 * HwCta<LPR>::W, SKMP_FIN_HW_MINB * 4 / HwCta<LPR>::W)
 finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, T* __restrict__ P,
                    int64_t* __restrict__ I) {
-  static_assert(SPAN <= 16 && (SPAN & (SPAN - 1)) == 0, "geometry");
-  using B = HwBuf<E, SPAN>;
-  __shared__ __align__(16) T fsm[kFinRegWarps * 4 * B::HS];
-  const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15;
-  T* hb = fsm + (threadIdx.x >> 5) * 4 * B::HS + h * B::HS;  // this half's buffer 0; buffer 1 at + 2 HS
-  const int64_t i_first = row_lo + ((int64_t)blockIdx.x * kFinRegWarps + (threadIdx.x >> 5)) * (2 * kFinRows);
+  static_assert(SPAN <= LPR && (SPAN & (SPAN - 1)) == 0, "geometry");
+  using B = HwBuf<T, E, LPR, SPAN>;
+  constexpr int G = 32 / LPR, WPC = HwCta<LPR>::W, VEC = B::VEC;
+  static_assert(E % VEC == 0, "E must be a multiple of the vector width");
+  __shared__ __align__(16) T fsm[WPC * 2 * G * B::HS];
+  const int lane = threadIdx.x & 31, grp = lane / LPR, l = lane % LPR;
+  T* gb = fsm + ((threadIdx.x >> 5) * 2 * G + grp) * B::HS;  // this group's buffer 0; buffer 1 at + G HS
+  const int64_t i_first = row_lo + ((int64_t)blockIdx.x * WPC + (threadIdx.x >> 5)) * (G * kFinRows);
   const int g = blockIdx.y;
   const int words = (w.dtype == SKMP_F32) ? 1 : 2;
   const int64_t* keys = w.keys + (int64_t)g * w.n_sub * words;
@@ -642,34 +667,34 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
   const double inf = __longlong_as_double(0x7ff0000000000000ll), nan = __longlong_as_double(0x7ff8000000000000ll);
   const int32_t nf = wo.nflat[g];
   const int32_t* F = wo.flat_list + (int64_t)g * wo.n_sub;
-  // half h walks rows i_first + 2 rr + h
-  auto row_of = [&](int rr) { const int64_t x = i_first + 2 * rr + h; return x < row_hi ? x : row_hi - 1; };
+  // group grp walks rows i_first + G rr + grp
+  auto row_of = [&](int rr) { const int64_t x = i_first + G * rr + grp; return x < row_hi ? x : row_hi - 1; };
   auto base_of = [&](int64_t kw) { int64_t kb = 0; return key_arg(kw, words, &kb) ? kb : (int64_t)0; };
+  const FinBase rbase{w.mu + o, w.isig64 + o, w.flat + o}, cbase{wo.mu + oo, wo.isig64 + oo, wo.flat + oo};
+  const int32_t nso = (int32_t)wo.n_sub;
+  // clamping b to [-32, n_sub] first keeps clamp(b + x, 0, n_sub - 1) for x < 32 (32-bit safe)
+  auto b32 = [nso](int64_t b) { return (int32_t)(b < -32 ? -32 : (b > nso ? (int64_t)nso : b)); };
   int64_t kw_cur = key_word(keys, row_of(0), words);
   int64_t kw_nxt = key_word(keys, row_of(1), words);
   {
-    T* wb = fsm + (threadIdx.x >> 5) * 4 * B::HS;
-    for (int q = lane; q < 4 * B::HS; q += 32) wb[q] = (T)0;  // tails stay zero
+    T* wb = fsm + (threadIdx.x >> 5) * 2 * G * B::HS;
+    for (int q = lane; q < 2 * G * B::HS; q += 32) wb[q] = (T)0;  // tails stay zero
   }
   __syncwarp();
-  const FinBase rbase{w.mu + o, w.isig64 + o, w.flat + o}, cbase{wo.mu + oo, wo.isig64 + oo, wo.flat + oo};
-  const int32_t nso = (int32_t)wo.n_sub;
-  // clamping b to [-32, n_sub] first keeps clamp(b + x, 0, n_sub - 1) for x < 16 (32-bit safe)
-  auto b32 = [nso](int64_t b) { return (int32_t)(b < -32 ? -32 : (b > nso ? (int64_t)nso : b)); };
-  hw_stage<T, E, SPAN, FULL>(hb, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, l);
+  hw_stage<T, E, LPR, SPAN, FULL>(gb, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, l);
   cp_async_commit();
-  FinPre pre = fin_pre32<SPAN>(rbase, cbase, (int32_t)row_of(0), b32(base_of(kw_cur)), nso, l);
+  FinPre pre = fin_pre32<SPAN, LPR>(rbase, cbase, (int32_t)row_of(0), b32(base_of(kw_cur)), nso, l);
   for (int rr = 0; rr < kFinRows; ++rr) {
-    const int64_t i_raw = i_first + 2 * rr + h;
+    const int64_t i_raw = i_first + G * rr + grp;
     const bool live = i_raw < row_hi;
     const int64_t i = row_of(rr);
     const int64_t kw = kw_cur;
     const FinPre cu = pre;
-    T* cur = hb + (rr & 1) * 2 * B::HS;
+    T* cur = gb + (rr & 1) * G * B::HS;
     if (rr + 1 < kFinRows) {
       const int64_t bn = base_of(kw_nxt);
-      hw_stage<T, E, SPAN, FULL>(hb + ((rr + 1) & 1) * 2 * B::HS, R, Ro, row_of(rr + 1), bn, m, wo.n, l);
-      pre = fin_pre32<SPAN>(rbase, cbase, (int32_t)row_of(rr + 1), b32(bn), nso, l);
+      hw_stage<T, E, LPR, SPAN, FULL>(gb + ((rr + 1) & 1) * G * B::HS, R, Ro, row_of(rr + 1), bn, m, wo.n, l);
+      pre = fin_pre32<SPAN, LPR>(rbase, cbase, (int32_t)row_of(rr + 1), b32(bn), nso, l);
     }
     cp_async_commit();
     kw_cur = kw_nxt;
@@ -681,31 +706,27 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
     const int64_t b = has ? kb : 0;
     const double mi = cu.mi;
     // ---- the SPAN candidate dot products over this lane's E positions -----------------------
-    const T* xi = cur + (E + 1) * l;           // position E l + e at (E+1) l + e
-    const T* xo = cur + B::XI + (E + 1) * l;   // position E l + t at (E+1) l + t + t / E
+    const T* xi = cur + (E + B::PAD) * l;           // position E l + e at (E + PAD) l + e
+    const T* xo = cur + B::XI + (E + B::PAD) * l;   // position E l + t at (E + PAD) l + t + PAD (t / E)
+    double a[E], wv[B::NW * VEC];
+#pragma unroll
+    for (int e = 0; e < E; e += VEC) ld_vec<T>(xi + e, a + e);
+#pragma unroll
+    for (int c = 0; c < B::NW; ++c) ld_vec<T>(xo + c * VEC + B::PAD * ((c * VEC) / E), wv + c * VEC);
     double acc[SPAN], asum = 0.0;
 #pragma unroll
     for (int d = 0; d < SPAN; ++d) acc[d] = 0.0;
-    double a[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int s = E * l + e;
-      a[e] = (FULL || s < m) ? (double)xi[e] - mi : 0.0;
+      a[e] = (FULL || E * l + e < m) ? a[e] - mi : 0.0;
       asum += a[e];
+#pragma unroll
+      for (int d = 0; d < SPAN; ++d) acc[d] = fma(a[e], wv[e + d], acc[d]);
     }
 #pragma unroll
-    for (int t = 0; t < E + SPAN - 1; ++t) {
-      const double wt = (double)xo[t + t / E];
-#pragma unroll
-      for (int d = 0; d < SPAN; ++d) {
-        const int e = t - d;
-        if (e >= 0 && e < E) acc[d] = fma(a[e], wt, acc[d]);
-      }
-    }
-#pragma unroll
-    for (int q = 8; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
-    xsum<SPAN, 16>(acc, l);
-    int d = xidx<SPAN, 16>(l);
+    for (int q = LPR / 2; q > 0; q >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, q);
+    xsum<SPAN, LPR>(acc, l);
+    int d = xidx<SPAN, LPR>(l);
     double dd = inf;
     const int64_t jd = b + d;
     if (admissible(i, jd, wo.n_sub, excl)) {
@@ -716,9 +737,9 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
         dd = 2.0 * m - (2.0 * cov) * (cu.ii * cu.ic);
       }
     }
-    // argmin over the SPAN candidates (16 / SPAN lanes of a half hold each)
+    // argmin over the SPAN candidates (LPR / SPAN lanes of a group hold each)
 #pragma unroll
-    for (int q = 8; q >= 16 / SPAN; q >>= 1) {
+    for (int q = LPR / 2; q >= LPR / SPAN; q >>= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, dd, q);
       const int oi = __shfl_xor_sync(0xffffffffu, d, q);
       if (od < dd || (od == dd && oi < d)) {
@@ -727,7 +748,7 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
       }
     }
     const int64_t jr = dd < inf ? b + d : -1;
-    const int src = (lane & 16) | xlane<SPAN, 16>(jr >= 0 ? d : 0);
+    const int src = grp * LPR + xlane<SPAN, LPR>(jr >= 0 ? d : 0);
     const double mj = __shfl_sync(0xffffffffu, cu.mc, src);
     const double ij = __shfl_sync(0xffffffffu, cu.ic, src);
     const bool fj = __shfl_sync(0xffffffffu, (int)cu.fc, src) != 0;
@@ -735,19 +756,19 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
     const int de = exact ? d : 0;
     double pe = sqrt(dd > 0.0 ? dd : 0.0);
     const bool need = exact && dd < kFinExplicitBelow;
-    if (__any_sync(0xffffffffu, need)) {  // whole warp (the reduction shuffles span both halves)
+    if (__any_sync(0xffffffffu, need)) {  // whole warp (the reduction shuffles span every group)
       const double ii = cu.ii;
       double acc2 = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int s = E * l + e;
         const double zi = __dmul_rn(a[e], ii);
-        const double zj = __dmul_rn((double)cur[B::XI + pad_pos<E>(s + de)] - mj, ij);
+        const double zj = __dmul_rn((double)cur[B::XI + B::padded(s + de)] - mj, ij);
         const double df = zi - zj;
         acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
       }
 #pragma unroll
-      for (int q = 8; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
+      for (int q = LPR / 2; q > 0; q >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, q);
       if (need) pe = sqrt(acc2);
     }
     double p;
@@ -793,6 +814,13 @@ bool fin_reg_enabled() {
 #ifndef SKMP_FIN_HW
 #define SKMP_FIN_HW 1
 #endif
+int fin_lpr() {
+  static const int v = [] {
+    const char* e = getenv("SKMP_FIN_LPR");  // lanes per row of the FP32 sub-warp kernel (A/B)
+    return (e && atoi(e) == 16) ? 16 : 8;
+  }();
+  return v;
+}
 bool fin_hw_enabled() {
   static const bool on = [] {
     const char* e = getenv("SKMP_FIN_IMPL");  // "reg": the full-warp register kernel (A/B)
@@ -812,28 +840,37 @@ cudaError_t launch_mp_finalize(const MpDev& w, const MpDev& wo, int excl, void* 
   const int nt = 32 * kFinWarps;
   const bool f32 = w.dtype == SKMP_F32;
 #define SKMP_FIN(TT, SP) finalize_kernel<TT, SP><<<grid, nt, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I)
-  // (FP64 windows longer than 128 keep the full-warp kernel: 16-position FP64 buffers exceed the
-  // static shared-memory limit)
+  // FP32: 8 lanes per row (E = m / 8 <= 32), or 16 with SKMP_FIN_LPR=16; FP64: 16 lanes per row
+  // (E <= 8); longer FP64 windows keep the full-warp kernel (the static shared-memory limit)
   if ((f32 ? w.m <= 256 : w.m <= 128) && (w.span == 4 || w.span == 8) && fin_hw_enabled()) {
-    const int Eh = w.m <= 64 ? 4 : (w.m <= 128 ? 8 : 16);
-    const int64_t perh = (int64_t)kFinRegWarps * 2 * kFinRows;
+    const int lpr = f32 ? fin_lpr() : 16;
+    const int Eh = (w.m + lpr - 1) / lpr <= 4 ? 4 : ((w.m + lpr - 1) / lpr <= 8 ? 8 : ((w.m + lpr - 1) / lpr <= 16 ? 16 : 32));
+    const int wpc = lpr == 8 ? HwCta<8>::W : HwCta<16>::W;
+    const int64_t perh = (int64_t)wpc * (32 / lpr) * kFinRows;
     grid.x = (unsigned)((row_hi - row_lo + perh - 1) / perh);
-    const int nth = 32 * kFinRegWarps;
-#define SKMP_FINH(TT, SP, EE)                                                                                   \
+    const int nth = 32 * wpc;
+#define SKMP_FINH(TT, SP, EE, LL)                                                                               \
   do {                                                                                                          \
-    if (w.m == 16 * (EE))                                                                                       \
-      finalize_hw_kernel<TT, SP, EE, true><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+    if (w.m == (LL) * (EE))                                                                                     \
+      finalize_hw_kernel<TT, SP, EE, LL, true><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
     else                                                                                                        \
-      finalize_hw_kernel<TT, SP, EE, false><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
+      finalize_hw_kernel<TT, SP, EE, LL, false><<<grid, nth, 0, st>>>(w, wo, excl, row_lo, row_hi, static_cast<TT*>(P), I); \
   } while (0)
-    if (w.span == 8) {
-      if (Eh == 4) { if (f32) SKMP_FINH(float, 8, 4); else SKMP_FINH(double, 8, 4); }
-      else if (Eh == 8) { if (f32) SKMP_FINH(float, 8, 8); else SKMP_FINH(double, 8, 8); }
-      else SKMP_FINH(float, 8, 16);
+    if (!f32) {
+      if (w.span == 8) { if (Eh == 4) SKMP_FINH(double, 8, 4, 16); else SKMP_FINH(double, 8, 8, 16); }
+      else { if (Eh == 4) SKMP_FINH(double, 4, 4, 16); else SKMP_FINH(double, 4, 8, 16); }
+    } else if (lpr == 16) {
+      if (w.span == 8) {
+        if (Eh == 4) SKMP_FINH(float, 8, 4, 16); else if (Eh == 8) SKMP_FINH(float, 8, 8, 16); else SKMP_FINH(float, 8, 16, 16);
+      } else {
+        if (Eh == 4) SKMP_FINH(float, 4, 4, 16); else if (Eh == 8) SKMP_FINH(float, 4, 8, 16); else SKMP_FINH(float, 4, 16, 16);
+      }
     } else {
-      if (Eh == 4) { if (f32) SKMP_FINH(float, 4, 4); else SKMP_FINH(double, 4, 4); }
-      else if (Eh == 8) { if (f32) SKMP_FINH(float, 4, 8); else SKMP_FINH(double, 4, 8); }
-      else SKMP_FINH(float, 4, 16);
+      if (w.span == 8) {
+        if (Eh <= 8) SKMP_FINH(float, 8, 8, 8); else if (Eh == 16) SKMP_FINH(float, 8, 16, 8); else SKMP_FINH(float, 8, 32, 8);
+      } else {
+        if (Eh <= 8) SKMP_FINH(float, 4, 8, 8); else if (Eh == 16) SKMP_FINH(float, 4, 16, 8); else SKMP_FINH(float, 4, 32, 8);
+      }
     }
 #undef SKMP_FINH
     count_launches(1);
