@@ -569,22 +569,52 @@ template <typename T, int E, int LPR, int SPAN> struct HwBuf {
   static constexpr int HS = XI + XO;                              // elements per row buffer
   static constexpr int NW = (E + SPAN - 1 + VEC - 1) / VEC;       // candidate vectors per lane
 };
+// FP32 with 8 lanes per row: the 4 rows of a warp are consecutive, so their row windows are one
+// super-window of m + 3 values staged once per warp (XR elements, same padding); each group keeps
+// its own candidate buffer (XO).  Per-warp stage size WS.
+#ifndef SKMP_FIN_SHR
+#define SKMP_FIN_SHR 1
+#endif
+template <typename T, int LPR> struct HwShared { static constexpr bool on = SKMP_FIN_SHR && sizeof(T) == 4 && LPR == 8; };
+template <typename T, int E, int LPR, int SPAN> struct HwLayout {
+  using B = HwBuf<T, E, LPR, SPAN>;
+  static constexpr int G = 32 / LPR;
+  static constexpr bool SHR = HwShared<T, LPR>::on;
+  static constexpr int XR = B::up(B::padded(LPR * E + G - 2) + 1);
+  static constexpr int WS = SHR ? XR + G * B::XO : G * B::HS;
+};
 template <int LPR> struct HwCta { static constexpr int W = LPR == 8 ? 2 : 4; };  // warps per CTA
 
 // stage row i's window and the candidate windows of base b into one group's buffer: lane l of
 // the group copies positions l + LPR q (padded: l + PAD (l / E) + LPR q + PAD ((LPR q) / E), a
 // lane base plus compile-time offsets); tails stay zero from the kernel start (see reg_stage)
 template <typename T, int E, int LPR, int SPAN, bool FULL>
-__device__ __forceinline__ void hw_stage(T* buf, const T* R, const T* Ro, int64_t i, int64_t b, int m,
-                                         int64_t n_o, int l) {
+__device__ __forceinline__ void hw_stage_row(T* xr, const T* R, int64_t i, int m, int l) {
   using B = HwBuf<T, E, LPR, SPAN>;
   static_assert(E % LPR == 0 || LPR % E == 0, "E and LPR must divide one another");
-  T* xi = buf + l + B::PAD * (l / E);
-  T* xo = buf + B::XI + l + B::PAD * (l / E);
+  T* xi = xr + l + B::PAD * (l / E);
   const T* gi = R + i + l;
 #pragma unroll
   for (int q = 0; q < E; ++q)
     if (FULL || l + LPR * q < m) cp_async_b(xi + LPR * q + B::PAD * ((LPR * q) / E), gi + LPR * q, (int)sizeof(T));
+}
+// the warp's shared row super-window: positions [i0, i0 + m + G - 1) of R (< n), lane-strided
+template <typename T, int E, int LPR, int SPAN>
+__device__ __forceinline__ void hw_stage_superrow(T* xr, const T* R, int64_t i0, int m, int64_t n, int lane) {
+  using B = HwBuf<T, E, LPR, SPAN>;
+  constexpr int G = 32 / LPR, NQ = (LPR * E + G - 1 + 31) / 32;
+  static_assert(32 % E == 0 || E % 32 == 0, "E and 32 must divide one another");
+  T* x = xr + lane + B::PAD * (lane / E);
+  const T* gi = R + i0 + lane;
+  const int lim = (int)((n - i0) < (int64_t)(m + G - 1) ? (n - i0) : (int64_t)(m + G - 1));
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (lane + 32 * q < lim) cp_async_b(x + 32 * q + B::PAD * ((32 * q) / E), gi + 32 * q, (int)sizeof(T));
+}
+template <typename T, int E, int LPR, int SPAN, bool FULL>
+__device__ __forceinline__ void hw_stage_cand(T* xc, const T* Ro, int64_t b, int m, int64_t n_o, int l) {
+  using B = HwBuf<T, E, LPR, SPAN>;
+  T* xo = xc + l + B::PAD * (l / E);
   const int no_used = FULL ? LPR * E + SPAN - 1 : m + SPAN - 1;  // (FULL: m = LPR E, compile-time masks)
   constexpr int NQ = (B::NO + LPR - 1) / LPR;
   if (b >= 0 && b + no_used <= n_o) {
@@ -650,11 +680,16 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
                    int64_t* __restrict__ I) {
   static_assert(SPAN <= LPR && (SPAN & (SPAN - 1)) == 0, "geometry");
   using B = HwBuf<T, E, LPR, SPAN>;
+  using Lay = HwLayout<T, E, LPR, SPAN>;
   constexpr int G = 32 / LPR, WPC = HwCta<LPR>::W, VEC = B::VEC;
+  constexpr bool SHR = Lay::SHR;
   static_assert(E % VEC == 0, "E must be a multiple of the vector width");
-  __shared__ __align__(16) T fsm[WPC * 2 * G * B::HS];
+  __shared__ __align__(16) T fsm[WPC * 2 * Lay::WS];
   const int lane = threadIdx.x & 31, grp = lane / LPR, l = lane % LPR;
-  T* gb = fsm + ((threadIdx.x >> 5) * 2 * G + grp) * B::HS;  // this group's buffer 0; buffer 1 at + G HS
+  T* wb0 = fsm + (threadIdx.x >> 5) * 2 * Lay::WS;  // this warp's stage 0; stage 1 at + WS
+  // row / candidate buffers of this group in stage k
+  auto rowbuf = [&](int k) { return wb0 + k * Lay::WS + (SHR ? 0 : grp * B::HS); };
+  auto candbuf = [&](int k) { return wb0 + k * Lay::WS + (SHR ? Lay::XR + grp * B::XO : grp * B::HS + B::XI); };
   const int64_t i_first = row_lo + ((int64_t)blockIdx.x * WPC + (threadIdx.x >> 5)) * (G * kFinRows);
   const int g = blockIdx.y;
   const int words = (w.dtype == SKMP_F32) ? 1 : 2;
@@ -676,12 +711,16 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
   auto b32 = [nso](int64_t b) { return (int32_t)(b < -32 ? -32 : (b > nso ? (int64_t)nso : b)); };
   int64_t kw_cur = key_word(keys, row_of(0), words);
   int64_t kw_nxt = key_word(keys, row_of(1), words);
-  {
-    T* wb = fsm + (threadIdx.x >> 5) * 2 * G * B::HS;
-    for (int q = lane; q < 2 * G * B::HS; q += 32) wb[q] = (T)0;  // tails stay zero
-  }
+  for (int q = lane; q < 2 * Lay::WS; q += 32) wb0[q] = (T)0;  // tails stay zero
   __syncwarp();
-  hw_stage<T, E, LPR, SPAN, FULL>(gb, R, Ro, row_of(0), base_of(kw_cur), m, wo.n, l);
+  // the warp's first row of step rr (SHR: the super-window's origin; group grp's row is at + r)
+  auto row0_of = [&](int rr) { const int64_t x = i_first + G * rr; return x < row_hi ? x : row_hi - 1; };
+  auto stage = [&](int k, int rr, int64_t bb) {
+    if constexpr (SHR) hw_stage_superrow<T, E, LPR, SPAN>(rowbuf(k), R, row0_of(rr), m, w.n, lane);
+    else hw_stage_row<T, E, LPR, SPAN, FULL>(rowbuf(k), R, row_of(rr), m, l);
+    hw_stage_cand<T, E, LPR, SPAN, FULL>(candbuf(k), Ro, bb, m, wo.n, l);
+  };
+  stage(0, 0, base_of(kw_cur));
   cp_async_commit();
   FinPre pre = fin_pre32<SPAN, LPR>(rbase, cbase, (int32_t)row_of(0), b32(base_of(kw_cur)), nso, l);
   for (int rr = 0; rr < kFinRows; ++rr) {
@@ -690,10 +729,11 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
     const int64_t i = row_of(rr);
     const int64_t kw = kw_cur;
     const FinPre cu = pre;
-    T* cur = gb + (rr & 1) * G * B::HS;
+    const T* crow = rowbuf(rr & 1);
+    const T* ccand = candbuf(rr & 1);
     if (rr + 1 < kFinRows) {
       const int64_t bn = base_of(kw_nxt);
-      hw_stage<T, E, LPR, SPAN, FULL>(gb + ((rr + 1) & 1) * G * B::HS, R, Ro, row_of(rr + 1), bn, m, wo.n, l);
+      stage((rr + 1) & 1, rr + 1, bn);
       pre = fin_pre32<SPAN, LPR>(rbase, cbase, (int32_t)row_of(rr + 1), b32(bn), nso, l);
     }
     cp_async_commit();
@@ -706,11 +746,20 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
     const int64_t b = has ? kb : 0;
     const double mi = cu.mi;
     // ---- the SPAN candidate dot products over this lane's E positions -----------------------
-    const T* xi = cur + (E + B::PAD) * l;           // position E l + e at (E + PAD) l + e
-    const T* xo = cur + B::XI + (E + B::PAD) * l;   // position E l + t at (E + PAD) l + t + PAD (t / E)
+    const T* xo = ccand + (E + B::PAD) * l;   // position E l + t at (E + PAD) l + t + PAD (t / E)
     double a[E], wv[B::NW * VEC];
+    if constexpr (SHR) {
+      // row position E l + e of group grp is super-window position r + E l + e, r = i - i0 < G:
+      // padded (E + PAD) l + r + e (+ PAD once r + e >= E, i.e. only for e >= E - G + 1)
+      const int r = (int)(i - row0_of(rr));
+      const T* xi = crow + (E + B::PAD) * l + r;
 #pragma unroll
-    for (int e = 0; e < E; e += VEC) ld_vec<T>(xi + e, a + e);
+      for (int e = 0; e < E; ++e) a[e] = (double)xi[e + (e >= E - G + 1 && r + e >= E ? B::PAD : 0)];
+    } else {
+      const T* xi = crow + (E + B::PAD) * l;  // position E l + e at (E + PAD) l + e
+#pragma unroll
+      for (int e = 0; e < E; e += VEC) ld_vec<T>(xi + e, a + e);
+    }
 #pragma unroll
     for (int c = 0; c < B::NW; ++c) ld_vec<T>(xo + c * VEC + B::PAD * ((c * VEC) / E), wv + c * VEC);
     double acc[SPAN], asum = 0.0;
@@ -763,7 +812,7 @@ finalize_hw_kernel(MpDev w, MpDev wo, int excl, int64_t row_lo, int64_t row_hi, 
       for (int e = 0; e < E; ++e) {
         const int s = E * l + e;
         const double zi = __dmul_rn(a[e], ii);
-        const double zj = __dmul_rn((double)cur[B::XI + B::padded(s + de)] - mj, ij);
+        const double zj = __dmul_rn((double)ccand[B::padded(s + de)] - mj, ij);
         const double df = zi - zj;
         acc2 = (FULL || s < m) ? __dadd_rn(acc2, __dmul_rn(df, df)) : acc2;
       }
