@@ -96,6 +96,43 @@ __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
 #ifndef SKMP_X2_RAWCOL
 #define SKMP_X2_RAWCOL 1
 #endif
+// next chunk's raw column records and row records staged by three 1-D bulk copies
+// (cp.async.bulk, TMA engine) issued by one lane and completed on an mbarrier, instead of three
+// 16-byte cp.asyncs per lane; the key words stay per-lane 4-byte cp.asyncs (strided)
+#ifndef SKMP_X2_BULK
+#define SKMP_X2_BULK 0
+#endif
+#if SKMP_X2_BULK && !(SKMP_X2_RAWCOL && SKMP_X2_ROWSCALAR)
+#error "SKMP_X2_BULK needs SKMP_X2_RAWCOL and SKMP_X2_ROWSCALAR"
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n"
+               "fence.mbarrier_init.release.cluster;\n"
+               "fence.proxy.async.shared::cta;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// the generic-proxy reads of a buffer (previous chunk) are ordered before the async-proxy writes
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{ .reg .pred p;\n"
+      "WAIT_%=:\n"
+      "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "  @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 struct __align__(16) ColRec0 { f2 df, dg; };   // {df_c, df_c+H}, {dg_c, dg_c+H}
 struct RowRec0 { f2 df, dg; };                 // {df_i, df_i}, {dg_i, dg_i}
 
@@ -245,7 +282,11 @@ __device__ __forceinline__ void row_keys(int u, f2 (&cov)[DG], const Col (&X)[DG
   for (int d = 0; d < DG; ++d) {
     const Col& x = X[(u + d) % DG];
     cov[d] = fma2(r0.df, x.dg, cov[d]);
+#if SKMP_X2_ROWFIRST
+    cov[d] = fma2(r0.dg, x.df, cov[d]);  // row operand in the first slot of both FFMA2s
+#else
     cov[d] = fma2(x.df, r0.dg, cov[d]);
+#endif
     const f2 rho = mul2(mul2(cov[d], x.inv), rinv);  // rho = cov inv_j inv_i (both groups)
     ka[d] = lo_of(rho);
     kb[d] = hi_of(rho);
@@ -402,7 +443,10 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
                                            int64_t n_sub_c, int e) {
   const uint32_t c = (uint32_t)c64, i = (uint32_t)i64;
   const uint32_t ns = (uint32_t)n_sub, nsc = (uint32_t)n_sub_c;
-#if SKMP_X2_RAWCOL
+#if SKMP_X2_BULK
+  (void)qc;
+  (void)q;
+#elif SKMP_X2_RAWCOL
   cp_async16(&sm->rawcA[e], qc + c);
   cp_async16(&sm->rawcB[e], qc + (c + H));
 #else
@@ -419,7 +463,9 @@ __device__ __forceinline__ void stage_next(Smem* sm, const float4* q, const int6
   cp_async4(d1 + 1, b + 2);
 #endif
   const int er = (int)(i & (2 * C - 1));
-#if SKMP_X2_ROWSCALAR
+#if SKMP_X2_BULK
+  (void)er;
+#elif SKMP_X2_ROWSCALAR
   cp_async16(&sm->rowq[er], q + i);  // the raw record, one 16-byte copy
 #else
   const float* r = reinterpret_cast<const float*>(q + i);
@@ -625,11 +671,29 @@ join_x2_kernel(JoinArgs a) {
   __shared__ int s_qt[NT];
   s_qt[tid] = (int)(((i0 + dt) % RS) / DG);
 #endif
+#if SKMP_X2_BULK
+  // rows i0 + C.. and columns are chunk-contiguous: i0 is a multiple of the tile length L (a
+  // multiple of 64, api.cu), so a chunk's row slots (i mod 2C) never wrap
+  __shared__ __align__(8) uint64_t s_bar;
+  if (tid == 0) mbar_init(&s_bar, 1);
+  __syncwarp();
+  uint32_t bar_ph = 0;
+#endif
 
   for (int64_t r = i0; r < i1; r += C) {
     const int64_t rend = (r + C < i1) ? r + C : i1;
     const bool more = r + C < i1;
     if (more) {
+#if SKMP_X2_BULK
+      if (tid == 0) {
+        const int64_t c0 = r + delta0 + H + C;
+        fence_async_smem();
+        mbar_expect_tx(&s_bar, 3 * C * (uint32_t)sizeof(float4));
+        bulk_g2s(sm.rawcA, qc + c0, C * sizeof(float4), &s_bar);
+        bulk_g2s(sm.rawcB, qc + (c0 + H), C * sizeof(float4), &s_bar);
+        bulk_g2s(&sm.rowq[(int)((r + C) & (2 * C - 1))], q + (r + C), C * sizeof(float4), &s_bar);
+      }
+#endif
 #pragma unroll
       for (int p = 0; p < CPT; ++p)
         stage_next(&sm, q, keys, qc, keysc, r + delta0 + H + C + tid + p * NT, r + C + tid + p * NT, n_sub,
@@ -665,6 +729,10 @@ join_x2_kernel(JoinArgs a) {
       rb = (rb + DG) & (2 * C - 1);
     }
     if (more) {
+#if SKMP_X2_BULK
+      mbar_wait(&s_bar, bar_ph);
+      bar_ph ^= 1;
+#endif
       cp_async_wait_all();
 #pragma unroll
       for (int p = 0; p < CPT; ++p) land_next(&sm, r + delta0 + H + C + tid + p * NT, r + C + tid + p * NT, tid + p * NT);
