@@ -78,3 +78,20 @@ def test_two_ranks_on_one_gpu_equal_one_rank(cuda, tmp_path, config, shape):
     assert np.array_equal(two["top"][:, :2], one["top"][:, :2]), (two["top"][:5], one["top"][:5])
     assert np.array_equal(two["dim"], one["dim"]) and np.array_equal(two["dim_score"], one["dim_score"])
     print(f"{config}: 2 ranks on one GPU == 1 rank (keys, P, I, top-{len(top)}, Alg. 3 j* = {int(two['dim'][0])})")
+
+
+def test_two_ranks_full_bench_line(cuda):
+    """The whole default bench path at N = 2 (incl. the pipelined e2e leg through pinned host
+    inputs and the max-over-ranks timing) runs and prints one complete JSON line."""
+    import json
+    args = ["--config", "c5", "--shape", "d=200,n=40000,k=8", "--steps", "2", "--warmup", "3", "--e2e-steps", "2",
+            "--no-cpu-baseline", "--backend", "gloo"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["roofline"]["frac"] > 0 and d["gpu_launches"] > 0
