@@ -206,6 +206,11 @@ __device__ __forceinline__ void rotation(T (&cov)[D], typename JT<T>::Q (&X)[D],
 #ifndef SKMP_F64_CELLTEST
 #define SKMP_F64_CELLTEST 1
 #endif
+// refresh the register copies of the column thresholds after a publish (1) or leave them stale
+// until the columns rotate out (0: no register shuffles around the publish branch)
+#ifndef SKMP_F64_XREFRESH
+#define SKMP_F64_XREFRESH 1
+#endif
 
 template <int D, int RSD_CT>
 __device__ __forceinline__ void publish_ct(int64_t* keys, int64_t* keysc, dq4* rowq, double2* h1, int rbu, int u, int qt,
@@ -234,15 +239,47 @@ __device__ __forceinline__ void publish_ct(int64_t* keys, int64_t* keysc, dq4* r
   }
   // the columns still in registers (s = u+1 .. u+D) take their current thresholds: a stale copy
   // would send the warp down this path again for cells that cannot improve the key
+#if SKMP_F64_XREFRESH
 #pragma unroll
   for (int s = u + 1; s <= u + D; ++s) X[s % D].w = h1[s < D ? s * RSD_CT + qt : (s - D) * RSD_CT + qt1].y;
+#else
+  (void)X;
+#endif
 }
 
 // hit |= (k >= t) for 16 (k, t) pairs with predicate-accumulating setp (written out in PTX:
 // from C++ the compiler fuses (k >= a) | (k >= b) into k >= min(a, b), a DSETP.MIN plus
-// NaN-fixing selects per cell)
+// NaN-fixing selects per cell).  SKMP_F64_CHAINS independent predicate chains, OR-ed at the end:
+// one chain makes the 16 DSETPs a serial dependency (each waits for the previous predicate at
+// FP64 latency), which left the block's tail stalled on `wait`
+#ifndef SKMP_F64_CHAINS
+#define SKMP_F64_CHAINS 4
+#endif
 __device__ __forceinline__ bool any_ge(const double (&k)[16], const double (&t)[16]) {
   unsigned r;
+#if SKMP_F64_CHAINS == 4
+  asm("{ .reg .pred p0, p1, p2, p3;\n"
+      "  setp.ge.f64 p0, %1, %17;\n"
+      "  setp.ge.f64 p1, %2, %18;\n"
+      "  setp.ge.f64 p2, %3, %19;\n"
+      "  setp.ge.f64 p3, %4, %20;\n"
+      "  setp.ge.or.f64 p0, %5, %21, p0;\n"
+      "  setp.ge.or.f64 p1, %6, %22, p1;\n"
+      "  setp.ge.or.f64 p2, %7, %23, p2;\n"
+      "  setp.ge.or.f64 p3, %8, %24, p3;\n"
+      "  setp.ge.or.f64 p0, %9, %25, p0;\n"
+      "  setp.ge.or.f64 p1, %10, %26, p1;\n"
+      "  setp.ge.or.f64 p2, %11, %27, p2;\n"
+      "  setp.ge.or.f64 p3, %12, %28, p3;\n"
+      "  setp.ge.or.f64 p0, %13, %29, p0;\n"
+      "  setp.ge.or.f64 p1, %14, %30, p1;\n"
+      "  setp.ge.or.f64 p2, %15, %31, p2;\n"
+      "  setp.ge.or.f64 p3, %16, %32, p3;\n"
+      "  or.pred p0, p0, p1;\n"
+      "  or.pred p2, p2, p3;\n"
+      "  or.pred p0, p0, p2;\n"
+      "  selp.u32 %0, 1, 0, p0; }"
+#else
   asm("{ .reg .pred p;\n"
       "  setp.ge.f64 p, %1, %17;\n"
       "  setp.ge.or.f64 p, %2, %18, p;\n"
@@ -261,6 +298,7 @@ __device__ __forceinline__ bool any_ge(const double (&k)[16], const double (&t)[
       "  setp.ge.or.f64 p, %15, %31, p;\n"
       "  setp.ge.or.f64 p, %16, %32, p;\n"
       "  selp.u32 %0, 1, 0, p; }"
+#endif
       : "=r"(r)
       : "d"(k[0]), "d"(k[1]), "d"(k[2]), "d"(k[3]), "d"(k[4]), "d"(k[5]), "d"(k[6]), "d"(k[7]), "d"(k[8]),
         "d"(k[9]), "d"(k[10]), "d"(k[11]), "d"(k[12]), "d"(k[13]), "d"(k[14]), "d"(k[15]), "d"(t[0]), "d"(t[1]),
@@ -308,7 +346,11 @@ __device__ __forceinline__ void rotation_ct(double (&cov)[D], dq4 (&X)[D], const
       tt[2 * D + 2 * d + 1] = x.w;
     }
     // ">=": exact ties reach the atomic (keys independent of tile order / band split)
-    if (__any_sync(0xffffffffu, any_ge(kk, tt)))
+    bool hit = any_ge(*reinterpret_cast<const double(*)[16]>(kk), *reinterpret_cast<const double(*)[16]>(tt));
+#pragma unroll
+    for (int q = 16; q < 4 * D; q += 16)
+      hit |= any_ge(*reinterpret_cast<const double(*)[16]>(kk + q), *reinterpret_cast<const double(*)[16]>(tt + q));
+    if (__any_sync(0xffffffffu, hit))
       publish_ct<D, RSD>(keys, keysc, rowq, rv.h1, rb + u, u, qt, (qt + 1 == RSD) ? 0 : qt + 1, ib + u, dt, ka, kb, X);
   }
 }
