@@ -6,3 +6,4 @@ for v in hw reg hw; do
   F=""; if [ "$v" = reg ]; then F=reg; fi
   SKMP_FIN_IMPL=$F timeout 600 python bench.py --config c4 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2_prep_$v.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/r2_prep_$v.json'));print('$v c4', round(d['ms_per_step'],2), {k: round(x,3) for k,x in d['phases_ms'].items()})"
 done 2>&1 | grep -v "^+"
+timeout 900 python -m pytest tests/test_gpu_multirank.py -q -x -k full_bench > gpurun_out/r2_multirank_e2e.log 2>&1; echo mr rc=$?; tail -30 gpurun_out/r2_multirank_e2e.log
