@@ -548,8 +548,17 @@ __device__ __forceinline__ void join_tile(const JoinArgs& a, int g, int64_t delt
 #ifndef SKMP_JOIN_MINB64
 #define SKMP_JOIN_MINB64 1
 #endif
-template <typename T, int D, int NT, int C>
-__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB : SKMP_JOIN_MINB64))
+// FP64 joins of a few waves (C1 / C2 sizes) are latency-bound: a second instance capped at 96
+// registers (18 resident warps instead of 16) runs them faster (C2-size join 2.89 -> 2.70 ms),
+// while larger FP64 joins keep the 114-register instance (n = 2e5: 174.5 vs 176.6 ms;
+// profiles/r2t_f64_occupancy.txt)
+#ifndef SKMP_JOIN_MINB64_SMALL
+#define SKMP_JOIN_MINB64_SMALL 18
+#endif
+constexpr int64_t kJoinSmallGrid = 16LL * 148 * 16;  // CTAs: <= 16 waves of 148 SMs x 16 warps
+template <typename T, int D, int NT, int C, bool SMALL = false>
+__global__ void __launch_bounds__(NT, ((sizeof(T) == 4 && D <= 8) ? SKMP_JOIN_MINB
+                                       : (SMALL ? SKMP_JOIN_MINB64_SMALL : SKMP_JOIN_MINB64)))
 join_kernel(JoinArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = NT * D;
@@ -564,17 +573,17 @@ join_kernel(JoinArgs a) {
   join_tile<T, D, NT, C, true>(a, g, delta0, i0, i1r, smem_raw);
 }
 
-template <typename T, int D>
+template <typename T, int D, bool SMALL = false>
 cudaError_t launch_join_t(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t dhi, const int64_t* prefix,
                           int64_t nblk, int64_t ntiles, int64_t blk0, cudaStream_t st) {
   constexpr int NT = kJoinNT, C = kJoinC;
   using G = Geo<T, D, NT, C>;
   const JoinArgs a = make_join_args(w, wc, dlo, dhi, prefix, nblk, blk0);
   const size_t smem = G::smem_bytes;
-  cudaError_t e = cudaFuncSetAttribute(join_kernel<T, D, NT, C>,
+  cudaError_t e = cudaFuncSetAttribute(join_kernel<T, D, NT, C, SMALL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
-  join_kernel<T, D, NT, C><<<(unsigned)(ntiles * w.k), NT, smem, st>>>(a);
+  join_kernel<T, D, NT, C, SMALL><<<(unsigned)(ntiles * w.k), NT, smem, st>>>(a);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -599,6 +608,8 @@ cudaError_t launch_mp_join(const MpDev& w, const MpDev& wc, int64_t dlo, int64_t
     if (join_d32() == 16) return launch_join_t<float, 16>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
     return launch_join_t<float, 8>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
   }
+  if (ntiles * w.k <= kJoinSmallGrid)
+    return launch_join_t<double, kJoinD64, true>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
   return launch_join_t<double, kJoinD64>(w, wc, dlo, dhi, d_prefix, nblk, ntiles, blk0, st);
 }
 

@@ -48,6 +48,14 @@ def test_mp_selfjoin_parity(cuda, dtype, n, m, k, kind, reseed):
     _run(cuda, X, m, dtype, reseed=reseed, label=f"{dtype} n={n} m={m}")
 
 
+def test_mp_f64_large_grid_instance(cuda):
+    """FP64 joins above 16 waves of CTAs run the 114-register kernel instance, smaller ones the
+    96-register instance (mp_join.cu kJoinSmallGrid): 64-row tiles give this n = 20,000 pair of
+    series ~49k CTAs, so the large instance is checked against the brute force too."""
+    X = synthgen.mp_series(2, 20000, seed=77, kind="mix")
+    _run(cuda, X, 50, "f64", reseed=64, label="f64 large grid")
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_mp_exclusion_zone_variants(cuda, dtype):
     X = synthgen.mp_series(1, 1500, seed=77, kind="mix")
